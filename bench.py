@@ -1,0 +1,380 @@
+"""Benchmark of the qDSE self-energy sweep (BASELINE.json metric:
+"qDSE integrand points/s (fp64, N_p*N_q*N_theta per iter); time-to-solution").
+
+Workload (N=1): BASELINE config 2 -- vacuum qDSE, Ball-Chiu vertex, fp64,
+N_p = N_q = 1024, N_theta = 256 (2.68e8 integrand points per iteration),
+A=1, B=0.3, xi=1e-10.  One step = one iteration of the on-device successive
+approximation loop (sweep of every external row + relaxation + max-norm
+convergence test) on device-resident state.  The reference does not converge
+on this grid, so the step is timed, not the solve; time to
+solution is reported for config 0 (2923 iterations) and for the convergent
+large substitute N=M=K=256, relaxation 0.5 (421 iterations).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference algorithm's CPU implementation (the C
+oracle port in oracle/, all host threads) on the same workload, a bounded
+row sample per step.  Under torchrun (N > 1) every rank owns the rows
+r, r+N, ... and the iterate is all-gathered over NCCL each step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "qDSE integrand points/s (fp64, N_p*N_q*N_theta per iter)"
+UNIT = "points/s"
+CFG2 = dict(N=1024, M=1024, K=256, p2_min=1e-6, p2_max=1e4)
+FLOP_PER_POINT = 55  # 47 add/sub/mul + 7 div + 1 exp, div/exp counted as 1
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _load_profile_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path)).get("dse_solve_kernel_bytes_per_launch")
+        except (OSError, ValueError):
+            return None
+    return None
+
+
+def cpu_port_rate(grid, params, budget_s: float, threads: int):
+    """Reference algorithm on the host: the C oracle (oracle/, a restatement of
+    row_rhs + np.sum order) over a row sample, all host threads."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    n, mk = grid.n_ext, grid.m_rad * grid.m_ang
+    a, b = np.ones(n), np.full(n, 0.3)
+    # calibrate on a few rows, then size the sample to ~budget_s
+    rows = max(threads, 8)
+    t0 = time.perf_counter()
+    oracle.sweep(grid, a, b, params, strategy=1, threads=threads, rows=(0, rows))
+    dt = time.perf_counter() - t0
+    per_row = dt / rows
+    take = int(min(n, max(threads, budget_s / max(per_row, 1e-9))))
+    t0 = time.perf_counter()
+    oracle.sweep(grid, a, b, params, strategy=1, threads=threads, rows=(0, take))  # oracle cost is row-uniform
+    dt = time.perf_counter() - t0
+    picked = np.arange(take)
+    pts = picked.size * mk
+    return pts / dt, {"rows": int(picked.size), "points": int(pts), "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return 0
+    import paper_2012_03667_b200 as p  # host grid builder only (numpy)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    threads = oracle.max_threads()
+    grid = p.build_grid(CFG2["N"], CFG2["M"], CFG2["K"], CFG2["p2_min"], CFG2["p2_max"])
+    params = p.ModelParams(N=1024, m_rad=1024, m_ang=256, xi=1e-10)
+    per_step = float(os.environ.get("BENCH_REF_STEP_S", "6.0"))
+    for _ in range(args.warmup):
+        cpu_port_rate(grid, params, min(per_step, 2.0), threads)
+    rates, info = [], None
+    for _ in range(args.steps):
+        r, info = cpu_port_rate(grid, params, per_step, threads)
+        rates.append(r)
+    value = float(np.mean(rates))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * CFG2["N"] * CFG2["M"] * CFG2["K"] / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "config2_vacuum_1024x1024x256", "N_p": 1024, "N_q": 1024, "N_theta": 256,
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{info['rows']} of 1024 external rows per step (full M*K block each), "
+                                   f"C oracle oracle/dse_oracle.c (row_rhs op order + numpy pairwise sum)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import paper_2012_03667_b200 as p
+    from paper_2012_03667_b200 import _native as nat
+
+    rank, world, local = _env_rank()
+    if world > 1:
+        return run_ours_distributed(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    os.environ["DSE_DEVICE"] = str(local)
+    gname, sms = nat.device_info(local)
+    grid = p.build_grid(CFG2["N"], CFG2["M"], CFG2["K"], CFG2["p2_min"], CFG2["p2_max"])
+    params = p.ModelParams(N=1024, m_rad=1024, m_ang=256, xi=1e-10)
+    arith = p.Arithmetic(args.arith)
+    sw = p.GpuSweeper(grid, params, p.InterpStrategy.PRECOMPUTED_INDEX, arith, local)
+    st = sw.stats()
+    n = grid.n_ext
+    A = torch.ones(n, dtype=torch.float64, device=dev)
+    B = torch.full((n,), 0.3, dtype=torch.float64, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    sptr = stream.cuda_stream
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # 256 MiB > 126 MB L2
+    params_tiny = params
+    with torch.cuda.stream(stream):
+        sw.load_device(A.data_ptr(), B.data_ptr(), sptr)
+        for _ in range(args.warmup):
+            flush.fill_(1)
+            sw.resume(1, sptr)
+        stream.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        launches0 = nat.launch_count()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            for e0, e1 in ev:
+                flush.fill_(1)               # L2 flush between timed iterations (not timed)
+                e0.record(stream)
+                sw.resume(1, sptr)           # one iteration: sweep + relax + convergence test
+                e1.record(stream)
+            stream.synchronize()
+        torch.cuda.synchronize()
+        launches = nat.launch_count() - launches0
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    t_total = sum(step_ms) / 1e3
+    nominal = st["nominal_points"]
+    value = nominal * args.steps / t_total
+    kernel_s = t_total / args.steps
+    peak = ctypes_fp64_peak(nat, local)
+    achieved = st["evaluated_points"] * FLOP_PER_POINT / kernel_s / 1e12
+
+    # e2e: public API with host buffers (H2D of A, B; D2H of A', B' every step)
+    a_h, b_h = np.ones(n), np.full(n, 0.3)
+    variant = p.VARIANTS["indexed-gpu"] if arith is p.Arithmetic.EXACT else p.VARIANTS["indexed-gpu-fast"]
+    for _ in range(2):
+        p.iterate_once(grid, a_h, b_h, params_tiny, variant)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a_c, b_c = a_h, b_h
+    for _ in range(args.steps):
+        a_c, b_c = p.iterate_once(grid, a_c, b_c, params_tiny, variant)
+    e2e_s = time.perf_counter() - t0
+    e2e = nominal * args.steps / e2e_s
+
+    extra = {}
+    if not args.no_tts:
+        extra["time_to_solution"] = time_to_solution(p, torch, dev, arith)
+    if not args.no_interp:
+        extra["interp_config1"] = interp_bench(p, nat, torch, dev, peak_hbm())
+    cpu = None
+    if not args.no_cpu:
+        rate, info = cpu_port_rate(grid, params, float(os.environ.get("BENCH_CPU_S", "10")),
+                                   _oracle_threads())
+        cpu = {"value": rate, "unit": UNIT, "cores": _oracle_threads(), "kind": "port",
+               "sample": f"{info['rows']} of 1024 external rows x full M*K block, one sweep "
+                         f"({info['points']:.3g} points, {info['seconds']:.1f} s), C oracle oracle/dse_oracle.c"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * kernel_s, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config2_vacuum_1024x1024x256", "N_p": 1024, "N_q": 1024, "N_theta": 256,
+                   "arith": arith.value, "interp": "indexed", "parallelism": "single GPU",
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "step": "one on-device iteration: sweep + relaxation + max-norm convergence test",
+                   "evaluated_points_per_step": st["evaluated_points"], "nominal_points_per_step": nominal},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": 2 * n * 8 + 32,
+                "api": "paper_2012_03667_b200.iterate_once(grid, A, B, params, VARIANTS['indexed-gpu'])"},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if peak else None, "traffic": _load_profile_traffic(),
+                     "flop_per_point": FLOP_PER_POINT, "points": "evaluated (exact-zero pairs skipped)",
+                     "peak_source": "measured: dse_fp64_peak DFMA probe on this GPU (MEASURED_PEAKS.json has no fp64)"},
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "device": gname,
+        **extra,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def _oracle_threads():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    return oracle.max_threads()
+
+
+_PEAK = None
+
+
+def ctypes_fp64_peak(nat, device):
+    global _PEAK
+    if _PEAK is None:
+        import ctypes
+        v = ctypes.c_double(0)
+        err = nat.DseErr()
+        nat.raise_for(nat.load().dse_fp64_peak(device, ctypes.byref(v), ctypes.byref(err)), err)
+        _PEAK = v.value
+    return _PEAK
+
+
+def peak_hbm():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback"
+
+
+def time_to_solution(p, torch, dev, arith):
+    out = {}
+    cases = {
+        "config0_128x128x64": (dict(N=128, m_rad=128, m_ang=64, xi=1e-10, max_iterations=20000), 1.0),
+        "substitute_256x256x256_relax0.5": (dict(N=256, m_rad=256, m_ang=256, xi=1e-10, max_iterations=2000,
+                                                 relaxation=0.5), 1.0),
+    }
+    for name, (kw, _) in cases.items():
+        prm = p.ModelParams(**kw)
+        g = p.build_grid(prm.N, prm.m_rad, prm.m_ang, prm.p2_min, prm.p2_max)
+        sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, arith)
+        A = torch.ones(prm.N, dtype=torch.float64, device=dev)
+        B = torch.full((prm.N,), 0.3, dtype=torch.float64, device=dev)
+        sw.solve_device(A.data_ptr(), B.data_ptr(), prm.max_iterations)  # warm-up
+        A.fill_(1.0)
+        B.fill_(0.3)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        it, conv = sw.solve_device(A.data_ptr(), B.data_ptr(), prm.max_iterations)
+        e1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        pts = sw.stats()["nominal_points"] * it
+        out[name] = {"iterations": it, "converged": conv, "seconds_device": e0.elapsed_time(e1) / 1e3,
+                     "seconds_wall": wall, "points_per_s": pts / wall}
+        sw.close()
+    return out
+
+
+def interp_bench(p, nat, torch, dev, hbm):
+    import ctypes
+    n = 1 << 26
+    x = np.logspace(-4, 4, 512)
+    v = 1.0 / (1.0 + x) + 0.1 * np.log1p(x)
+    q = np.exp(np.random.default_rng(0).uniform(np.log(1e-4), np.log(1e4), n))
+    dx = torch.from_numpy(x).to(dev)
+    dv = torch.from_numpy(v).to(dev)
+    dq = torch.from_numpy(q).to(dev)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    idx = torch.empty(n, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    lib = nat.load()
+    res = {}
+    for mode_name, mode in (("search", nat.BATCH_SEARCH), ("direct", nat.BATCH_DIRECT)):
+        ts = []
+        for r in range(8):
+            flush.fill_(0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            err = nat.DseErr()
+            s = torch.cuda.current_stream().cuda_stream
+            e0.record()
+            rc = lib.dse_interp_linear_batch_device(dx.data_ptr(), dv.data_ptr(), 512, dq.data_ptr(), n, mode,
+                                                    out.data_ptr(), idx.data_ptr(), s, ctypes.byref(err))
+            e1.record()
+            nat.raise_for(rc, err)
+            torch.cuda.synchronize()
+            if r >= 2:
+                ts.append(e0.elapsed_time(e1) / 1e3)
+        t = float(np.median(ts))
+        gbs = n * 20 / t / 1e9
+        res[mode_name] = {"queries_per_s": n / t, "seconds": t, "achieved_gbs": gbs,
+                          "frac_hbm": gbs / hbm[0], "peak_gbs": hbm[0], "peak_source": hbm[1],
+                          "bytes_per_query": 20}
+    t0 = time.perf_counter()
+    p.interp_linear_batch(x, v, q, mode="direct")
+    res["e2e_host_arrays_queries_per_s"] = n / (time.perf_counter() - t0)
+    return res
+
+
+def run_ours_distributed(args):
+    from paper_2012_03667_b200 import distributed as D
+    return D.bench_main(args, METRIC, UNIT, CFG2, FLOP_PER_POINT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--arith", choices=["exact", "fast"], default=os.environ.get("DSE_BENCH_ARITH", "exact"))
+    ap.add_argument("--no-tts", action="store_true")
+    ap.add_argument("--no-interp", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

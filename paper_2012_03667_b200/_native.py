@@ -1,0 +1,138 @@
+"""ctypes binding of libdse_b200.so (include/dse_b200.h).
+
+The library is built in-tree by paper_2012_03667_b200._build (nvcc, sm_100a).
+There is no CPU fallback: if the library or a B200 is missing, every call
+raises ExecutionEnvironmentError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import ExecutionEnvironmentError, NumericalFailureError, ParameterError
+
+LIB_NAME = "libdse_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+DSE_OK, DSE_EPARAM, DSE_ENUMERIC, DSE_EENV = 0, 1, 2, 3
+INTERP_SEARCH, INTERP_INDEXED = 0, 1
+BATCH_SEARCH, BATCH_DIRECT = 0, 1
+ARITH_EXACT, ARITH_FAST = 0, 1
+
+f64p = ctypes.POINTER(ctypes.c_double)
+i64p = ctypes.POINTER(ctypes.c_int64)
+i32p = ctypes.POINTER(ctypes.c_int32)
+
+
+class DseGrid(ctypes.Structure):
+    _fields_ = [("p2_ext", f64p), ("q2_int", f64p), ("sqrt_q2_int", f64p), ("radial_measure", f64p),
+                ("bracket_idx", i64p), ("z_nodes", f64p), ("z_weights", f64p),
+                ("n_ext", ctypes.c_int64), ("m_rad", ctypes.c_int64), ("m_ang", ctypes.c_int64)]
+
+
+class DseParams(ctypes.Structure):
+    _fields_ = [("coeff", ctypes.c_double), ("omega", ctypes.c_double), ("m0", ctypes.c_double),
+                ("z1", ctypes.c_double), ("xi", ctypes.c_double), ("relaxation", ctypes.c_double),
+                ("max_iterations", ctypes.c_int64)]
+
+
+class DseErr(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_int32), ("iteration", ctypes.c_int64), ("row", ctypes.c_int64),
+                ("radial", ctypes.c_int64), ("angular", ctypes.c_int64), ("msg", ctypes.c_char * 256)]
+
+
+_LIB = None
+
+# (name, restype, argtypes) -- one row per declaration in include/dse_b200.h
+_PROTOS = [
+    ("dse_device_info", ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(DseErr)]),
+    ("dse_sweeper_create", ctypes.c_int, [ctypes.POINTER(DseGrid), ctypes.POINTER(DseParams), ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(DseErr)]),
+    ("dse_sweeper_destroy", ctypes.c_int, [ctypes.c_void_p]),
+    ("dse_sweeper_sweep", ctypes.c_int, [ctypes.c_void_p, f64p, f64p, f64p, f64p, ctypes.POINTER(DseErr)]),
+    ("dse_sweeper_sweep_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                                ctypes.POINTER(DseErr)]),
+    ("dse_sweeper_check", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DseErr)]),
+    ("dse_solve", ctypes.c_int, [ctypes.c_void_p, f64p, ctypes.c_int64, f64p, f64p, i64p,
+                                 ctypes.POINTER(ctypes.c_int), f64p, ctypes.POINTER(DseErr)]),
+    ("dse_solve_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                        i64p, ctypes.POINTER(ctypes.c_int), ctypes.c_size_t,
+                                        ctypes.POINTER(DseErr)]),
+    ("dse_interp_indexed_batch", ctypes.c_int, [f64p, f64p, ctypes.c_int64, f64p, i64p, ctypes.c_int64, f64p,
+                                                ctypes.POINTER(DseErr)]),
+    ("dse_interp_linear_batch", ctypes.c_int, [f64p, f64p, ctypes.c_int64, f64p, ctypes.c_int64, ctypes.c_int,
+                                               f64p, i32p, i64p, ctypes.POINTER(DseErr)]),
+    ("dse_interp_linear_batch_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                                      ctypes.POINTER(DseErr)]),
+    ("dse_solve_load", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                      ctypes.POINTER(DseErr)]),
+    ("dse_solve_resume", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
+    ("dse_sweeper_stats", ctypes.c_int, [ctypes.c_void_p, i64p, i64p, i64p, i32p, i64p]),
+    ("dse_fp64_peak", ctypes.c_int, [ctypes.c_int, f64p, ctypes.POINTER(DseErr)]),
+    ("dse_launch_count", ctypes.c_int64, []),
+]
+
+EXPORTED_SYMBOLS = tuple(p[0] for p in _PROTOS)
+
+
+def load(path: str = LIB_PATH):
+    """Load the CUDA library (once).  Raises ExecutionEnvironmentError if absent."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise ExecutionEnvironmentError(
+            f"{LIB_NAME} is not built ({path}); run `python -c \"import __graft_entry__ as g; g.build()\"`")
+    try:
+        lib = ctypes.CDLL(path)
+    except OSError as exc:
+        raise ExecutionEnvironmentError(f"cannot load {path}: {exc}") from exc
+    for name, res, args in _PROTOS:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def raise_for(rc: int, err: DseErr) -> None:
+    """Map a C-ABI return code onto the reference's exception classes."""
+    if rc == DSE_OK:
+        return
+    msg = err.msg.decode(errors="replace")
+    if rc == DSE_EPARAM:
+        raise ParameterError(msg)
+    if rc == DSE_ENUMERIC:
+        raise NumericalFailureError(msg, row=int(err.row), radial=int(err.radial), angular=int(err.angular),
+                                    iteration=int(err.iteration) or None)
+    raise ExecutionEnvironmentError(msg or f"CUDA library error {rc}")
+
+
+def device_info(device: int = 0):
+    lib = load()
+    name = ctypes.create_string_buffer(128)
+    sms = ctypes.c_int(0)
+    err = DseErr()
+    raise_for(lib.dse_device_info(device, name, 128, ctypes.byref(sms), ctypes.byref(err)), err)
+    return name.value.decode(), sms.value
+
+
+def as_f64(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(f64p)
+
+
+def as_i64(a):
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    return a, a.ctypes.data_as(i64p)
+
+
+def launch_count() -> int:
+    return int(load().dse_launch_count())

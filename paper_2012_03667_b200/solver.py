@@ -1,0 +1,353 @@
+"""Gap-equation solver on the GPU (drop-in for reference solver.py:1-266).
+
+Same entry points, signatures and return types as the reference:
+
+  solve(params, variant, grid=None, probes_log10p=(-2.5, 0.0), a0=None, b0=None)
+      -> PropagatorSolution                                   (solver.py:221-266)
+  iterate_once(grid, a, b, params, variant) -> (A', B')      (solver.py:201-212)
+
+The strategy seam is kept: AlgorithmVariant(interp, execution, threads) and
+_make_sweeper (solver.py:53-74, 195-198).  The only execution mode is
+ExecutionMode.GPU; the reference's four variant names resolve to the GPU
+variant with the same interpolation strategy, so caller code written against
+dsegap runs unchanged.  `solve` hands the whole successive-approximation loop
+to the device (dse_solve): relaxation, max-norm deltas, the strict stopping
+rule, history and probes all happen in the persistent kernel, with no host
+round trip per iteration.
+
+Multi-GPU (variant.threads = G > 1): see paper_2012_03667_b200.distributed.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+import threading
+from collections import OrderedDict
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ParameterError
+from .grid import MomentumGrid, build_grid
+from .interpolation import InterpStrategy
+from .kernels import ModelParams
+
+__all__ = [
+    "ExecutionMode",
+    "Arithmetic",
+    "AlgorithmVariant",
+    "VARIANTS",
+    "IterationRecord",
+    "PropagatorSolution",
+    "resolve_threads",
+    "iterate_once",
+    "solve",
+    "GpuSweeper",
+    "DEFAULT_PROBES_LOG10P",
+]
+
+THREADS_ENV_VAR = "SOLVER_THREADS"
+DEVICE_ENV_VAR = "DSE_DEVICE"
+
+DEFAULT_PROBES_LOG10P = (-2.5, 0.0)
+
+
+class ExecutionMode(enum.Enum):
+    GPU = "gpu"
+
+
+class Arithmetic(enum.Enum):
+    """How the integrand is evaluated on the device.
+
+    EXACT: the reference's operation order (kernels.py:188-218), one rounding
+           per numpy op, IEEE divides; differs from the reference only by the
+           device exp (<= 1 ulp).
+    FAST:  algebraically reduced, FMA-contracted, one reciprocal of k2 per
+           point (csrc/dse_device.cuh point_fast).
+    """
+
+    EXACT = "exact"
+    FAST = "fast"
+
+
+@dataclass(frozen=True)
+class AlgorithmVariant:
+    """(interpolation strategy x execution) cell; threads = GPUs per solve."""
+
+    interp: InterpStrategy
+    execution: ExecutionMode = ExecutionMode.GPU
+    threads: int | None = None
+    arith: Arithmetic = Arithmetic.EXACT
+
+    @property
+    def name(self) -> str:
+        base = f"{self.interp.value}-{self.execution.value}"
+        return base if self.arith is Arithmetic.EXACT else f"{base}-{self.arith.value}"
+
+    def with_threads(self, threads: int | None) -> "AlgorithmVariant":
+        return AlgorithmVariant(self.interp, self.execution, threads, self.arith)
+
+    def with_arith(self, arith: Arithmetic) -> "AlgorithmVariant":
+        return AlgorithmVariant(self.interp, self.execution, self.threads, arith)
+
+
+_SEARCH = AlgorithmVariant(InterpStrategy.SEARCH_BASED)
+_INDEXED = AlgorithmVariant(InterpStrategy.PRECOMPUTED_INDEX)
+
+VARIANTS = {
+    "search-gpu": _SEARCH,
+    "indexed-gpu": _INDEXED,
+    "search-gpu-fast": _SEARCH.with_arith(Arithmetic.FAST),
+    "indexed-gpu-fast": _INDEXED.with_arith(Arithmetic.FAST),
+    # the reference's names (solver.py:69-74) -> the GPU variant with that strategy
+    "search-seq": _SEARCH,
+    "indexed-seq": _INDEXED,
+    "search-par": _SEARCH,
+    "indexed-par": _INDEXED,
+}
+
+
+@dataclass(frozen=True)
+class IterationRecord:
+    iteration: int
+    max_delta_a: float
+    max_delta_b: float
+    probe_a: tuple[float, ...]
+    probe_b: tuple[float, ...]
+
+
+@dataclass
+class PropagatorSolution:
+    A: np.ndarray
+    B: np.ndarray
+    iterations: int
+    converged: bool
+    history: list[IterationRecord]
+    grid: MomentumGrid
+    params: ModelParams
+    probes_log10p: tuple[float, ...] = field(default=DEFAULT_PROBES_LOG10P)
+
+
+def resolve_threads(variant: AlgorithmVariant) -> int:
+    """GPU count of a variant: variant.threads, else $SOLVER_THREADS, else 1."""
+    if variant.threads is not None:
+        n = variant.threads
+    else:
+        env = os.environ.get(THREADS_ENV_VAR)
+        n = int(env) if env else 1
+    if n < 1:
+        raise ParameterError(f"thread count must be >= 1, got {n}")
+    return n
+
+
+def _device() -> int:
+    env = os.environ.get(DEVICE_ENV_VAR)
+    if env:
+        return int(env)
+    try:
+        import torch  # optional: follow the caller's current device when torch is in use
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            return torch.cuda.current_device()
+    except Exception:  # noqa: BLE001
+        pass
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def _c_params(params: ModelParams) -> nat.DseParams:
+    return nat.DseParams(float(params.interaction_coeff), float(params.omega), float(params.m0),
+                         float(params.z1), float(params.xi), float(params.relaxation),
+                         int(params.max_iterations))
+
+
+class GpuSweeper:
+    """Device-resident sweeper (the _SequentialSweeper/_ParallelSweeper seam,
+    solver.py:148-192): grid uploaded once, sweep(a, b) -> (a', b'), close().
+
+    rows = (start, stride) restricts the sweeper to external rows
+    start, start+stride, ... (multi-GPU row sharding)."""
+
+    def __init__(self, grid, params: ModelParams, strategy: InterpStrategy,
+                 arith: Arithmetic = Arithmetic.EXACT, device: int | None = None,
+                 rows: tuple[int, int] = (0, 1)):
+        self.lib = nat.load()
+        self.grid = grid
+        self.params = params
+        self.n = grid.n_ext
+        self.device = _device() if device is None else device
+        keep = [nat.as_f64(grid.p2_ext), nat.as_f64(grid.q2_int), nat.as_f64(grid.sqrt_q2_int),
+                nat.as_f64(grid.radial_measure), nat.as_i64(grid.bracket_idx), nat.as_f64(grid.z_nodes),
+                nat.as_f64(grid.z_weights)]
+        g = nat.DseGrid(*(p for _, p in keep), grid.n_ext, grid.m_rad, grid.m_ang)
+        prm = _c_params(params)
+        handle = ctypes.c_void_p()
+        err = nat.DseErr()
+        strat = nat.INTERP_INDEXED if strategy is InterpStrategy.PRECOMPUTED_INDEX else nat.INTERP_SEARCH
+        ar = nat.ARITH_FAST if arith is Arithmetic.FAST else nat.ARITH_EXACT
+        rc = self.lib.dse_sweeper_create(ctypes.byref(g), ctypes.byref(prm), strat, ar, self.device,
+                                         int(rows[0]), int(rows[1]), ctypes.byref(handle), ctypes.byref(err))
+        nat.raise_for(rc, err)
+        self.handle = handle
+        self._lock = threading.Lock()
+
+    def sweep(self, a, b):
+        a, pa = nat.as_f64(a)
+        b, pb = nat.as_f64(b)
+        ao = np.empty(self.n)
+        bo = np.empty(self.n)
+        err = nat.DseErr()
+        with self._lock:
+            rc = self.lib.dse_sweeper_sweep(self.handle, pa, pb, ao.ctypes.data_as(nat.f64p),
+                                            bo.ctypes.data_as(nat.f64p), ctypes.byref(err))
+        nat.raise_for(rc, err)
+        return ao, bo
+
+    def sweep_device(self, dA: int, dB: int, dA_out: int, dB_out: int, stream: int = 0) -> None:
+        """One sweep on device buffers (raw pointers, e.g. torch .data_ptr())."""
+        err = nat.DseErr()
+        rc = self.lib.dse_sweeper_sweep_device(self.handle, dA, dB, dA_out, dB_out, stream, ctypes.byref(err))
+        nat.raise_for(rc, err)
+
+    def check(self) -> None:
+        err = nat.DseErr()
+        nat.raise_for(self.lib.dse_sweeper_check(self.handle, ctypes.byref(err)), err)
+
+    def solve(self, a0, b0, probes_p2=()):
+        """Whole successive-approximation loop on the device (dse_solve)."""
+        a = np.array(a0, dtype=np.float64, copy=True)
+        b = np.array(b0, dtype=np.float64, copy=True)
+        pr, ppr = nat.as_f64(np.asarray(probes_p2, dtype=np.float64).reshape(-1))
+        cap = int(self.params.max_iterations)
+        hist = np.empty((cap + 1, 3 + 2 * pr.size))
+        it = ctypes.c_int64(0)
+        conv = ctypes.c_int(0)
+        err = nat.DseErr()
+        with self._lock:
+            rc = self.lib.dse_solve(self.handle, ppr, pr.size, a.ctypes.data_as(nat.f64p),
+                                    b.ctypes.data_as(nat.f64p), ctypes.byref(it), ctypes.byref(conv),
+                                    hist.ctypes.data_as(nat.f64p), ctypes.byref(err))
+        nat.raise_for(rc, err)
+        n = int(it.value)
+        return a, b, n, bool(conv.value), hist[: n + 1]
+
+    def solve_device(self, dA: int, dB: int, max_iterations: int, stream: int = 0, wait: bool = True):
+        """Device-resident loop on raw device pointers (benchmarks)."""
+        err = nat.DseErr()
+        it = ctypes.c_int64(0)
+        conv = ctypes.c_int(0)
+        rc = self.lib.dse_solve_device(self.handle, dA, dB, int(max_iterations),
+                                       ctypes.byref(it) if wait else None, ctypes.byref(conv) if wait else None,
+                                       stream, ctypes.byref(err))
+        nat.raise_for(rc, err)
+        return (int(it.value), bool(conv.value)) if wait else None
+
+    def load_device(self, dA: int, dB: int, stream: int = 0) -> None:
+        """Copy device A/B into the resident state and rewind to iteration 0."""
+        err = nat.DseErr()
+        nat.raise_for(self.lib.dse_solve_load(self.handle, dA, dB, stream, ctypes.byref(err)), err)
+
+    def resume(self, n_iterations: int, stream: int = 0) -> None:
+        """Run the next n_iterations of the on-device loop (one launch, async)."""
+        err = nat.DseErr()
+        nat.raise_for(self.lib.dse_solve_resume(self.handle, int(n_iterations), stream, ctypes.byref(err)), err)
+
+    def stats(self) -> dict:
+        nom, ev, rows, smem = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        blocks = ctypes.c_int32()
+        self.lib.dse_sweeper_stats(self.handle, ctypes.byref(nom), ctypes.byref(ev), ctypes.byref(rows),
+                                   ctypes.byref(blocks), ctypes.byref(smem))
+        return {"nominal_points": nom.value, "evaluated_points": ev.value, "rows": rows.value,
+                "blocks": blocks.value, "smem_bytes": smem.value}
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.dse_sweeper_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+# iterate_once builds a sweeper per call in the reference (solver.py:208); the
+# device upload is cached per (grid, params, strategy) so repeated calls only
+# move A and B.
+_CACHE: "OrderedDict[tuple, GpuSweeper]" = OrderedDict()
+_CACHE_MAX = 4
+_CACHE_LOCK = threading.Lock()
+
+
+def _params_key(p: ModelParams):
+    return (p.D, p.omega, p.m0, p.z1, p.xi, p.relaxation, p.max_iterations)
+
+
+def _make_sweeper(grid, params, variant: AlgorithmVariant) -> GpuSweeper:
+    if variant.execution is not ExecutionMode.GPU:
+        raise ParameterError(f"unsupported execution mode {variant.execution}")
+    dev = _device()
+    key = (id(grid), _params_key(params), variant.interp, variant.arith, dev)
+    with _CACHE_LOCK:
+        hit = _CACHE.get(key)
+        if hit is not None and hit.grid is grid:
+            _CACHE.move_to_end(key)
+            return hit
+        sw = GpuSweeper(grid, params, variant.interp, variant.arith, dev)
+        _CACHE[key] = sw
+        while len(_CACHE) > _CACHE_MAX:
+            _, old = _CACHE.popitem(last=False)
+            old.close()
+        return sw
+
+
+def clear_sweeper_cache() -> None:
+    with _CACHE_LOCK:
+        while _CACHE:
+            _CACHE.popitem()[1].close()
+
+
+def iterate_once(grid: MomentumGrid, a: np.ndarray, b: np.ndarray, params: ModelParams,
+                 variant: AlgorithmVariant):
+    """One Jacobi sweep (A', B') from (A, B) on the GPU (solver.py:201-212)."""
+    a = np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    if a.shape != (grid.n_ext,) or b.shape != (grid.n_ext,):
+        raise ParameterError("A and B must match the external grid size")
+    if resolve_threads(variant) > 1:
+        from .distributed import iterate_once_sharded
+        return iterate_once_sharded(grid, a, b, params, variant)
+    return _make_sweeper(grid, params, variant).sweep(a, b)
+
+
+def solve(params: ModelParams, variant: AlgorithmVariant, grid: MomentumGrid | None = None,
+          probes_log10p: tuple[float, ...] = DEFAULT_PROBES_LOG10P, a0: np.ndarray | None = None,
+          b0: np.ndarray | None = None) -> PropagatorSolution:
+    """Iterate from A = B = 1 (or a0/b0) until both max-norm updates drop below
+    xi, on the device; converged=False (not an error) at the iteration cap
+    (solver.py:221-266, iteration.py:18-40)."""
+    params.validate()
+    if grid is None:
+        grid = build_grid(params.N, params.m_rad, params.m_ang, params.p2_min, params.p2_max)
+    probes_p2 = tuple(10.0 ** (2.0 * lp) for lp in probes_log10p)
+    a = np.ones(grid.n_ext) if a0 is None else np.asarray(a0, dtype=float).copy()
+    b = np.ones(grid.n_ext) if b0 is None else np.asarray(b0, dtype=float).copy()
+    if a.shape != (grid.n_ext,) or b.shape != (grid.n_ext,):
+        raise ParameterError("a0 and b0 must match the external grid size")
+    if resolve_threads(variant) > 1:
+        from .distributed import solve_sharded
+        a, b, n, conv, hist = solve_sharded(grid, params, variant, a, b, probes_p2)
+    else:
+        sweeper = _make_sweeper(grid, params, variant)
+        a, b, n, conv, hist = sweeper.solve(a, b, probes_p2)
+    P = len(probes_p2)
+    history = [IterationRecord(int(r[0]), float(r[1]), float(r[2]), tuple(float(x) for x in r[3:3 + P]),
+                               tuple(float(x) for x in r[3 + P:3 + 2 * P])) for r in hist]
+    return PropagatorSolution(A=a, B=b, iterations=n, converged=conv, history=history, grid=grid,
+                              params=params, probes_log10p=tuple(probes_log10p))
+
+
+def _row_rhs_gpu(p2, a_p, b_p, a_q, b_q, grid, params, row):
+    raise NotImplementedError("row_rhs on an arbitrary (a_q, b_q) is served by the sweep; "
+                              "use iterate_once for full rows")

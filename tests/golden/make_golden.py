@@ -1,0 +1,242 @@
+"""Generate the golden fixtures in tests/golden/ by RUNNING THE REFERENCE.
+
+The reference (`dsegap`, pure Python + numpy) is imported read-only from
+/root/reference/pkg/src.  This script is run once in the build container
+(the reference does not exist on the GPU box); its outputs are committed:
+
+  grid_<tag>.npz      build_grid(...) arrays (pins our host grid builder bitwise)
+  sweep_<tag>.npz     iterate_once(...) on seeded inputs (pins the sweep)
+  solve_c0.npz        config 0 solve: 2923 iterations, A, B, full history
+  solve_c2k10.npz     config 2 (1024/1024/256) first 10 sweeps
+  solve_sub256.npz    convergent large substitute N=M=K=256, relaxation 0.5
+  interp_c1.npz       config 1 interpolation on a 2**16-query sample
+  errors.npz          NumericalFailureError locations
+
+Usage:  python tests/golden/make_golden.py [--only NAME ...] [--threads C]
+Which reference call produced each file is recorded inside it (`call`).
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+import dsegap  # noqa: E402
+from dsegap import (VARIANTS, ModelParams, NumericalFailureError, build_grid,  # noqa: E402
+                    interp_search_many, iterate_once, solve)
+from dsegap.interpolation import _bracket_search  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def grid_arrays(g):
+    return dict(p2_ext=g.p2_ext, s_nodes=g.s_nodes, s_weights=g.s_weights, q2_int=g.q2_int,
+                bracket_idx=g.bracket_idx, z_nodes=g.z_nodes, z_weights=g.z_weights,
+                sqrt_q2_int=g.sqrt_q2_int, radial_measure=g.radial_measure)
+
+
+def save(name, **kw):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **kw)
+    print(f"wrote {path} ({os.path.getsize(path)} B)")
+
+
+GRIDS = {
+    # tag: (N, M, K, p2_min, p2_max)
+    "c0": (128, 128, 64, 1e-6, 1e4),          # config 0 (SURVEY F1 mapping)
+    "default": (150, 100, 32, 1e-6, 1e4),     # ModelParams defaults (kernels.py:46-57)
+    "small": (20, 16, 8, 1e-6, 1e4),
+    "ragged": (37, 29, 5, 1e-4, 1e3),         # sizes that are not multiples of 8
+    "tiny": (2, 2, 1, 1e-2, 1e2),             # minimum sizes allowed by validate()
+    "coincide": (3, 3, 2, 1.0, 9.0),          # exercises the coincidence shift (grid.py:122-130)
+    "sub256": (256, 256, 256, 1e-6, 1e4),
+    "c2": (1024, 1024, 256, 1e-6, 1e4),
+}
+
+
+def make_grids():
+    for tag, (n, m, k, lo, hi) in GRIDS.items():
+        g = build_grid(n, m, k, lo, hi)
+        save(f"grid_{tag}.npz", args=np.array([n, m, k]), p2_range=np.array([lo, hi]),
+             call=f"build_grid({n},{m},{k},{lo},{hi})", **grid_arrays(g))
+
+
+def make_sweeps():
+    rng = np.random.default_rng(20240601)
+    cases = []
+    for tag in ("c0", "default", "small", "ragged", "tiny"):
+        n, m, k, lo, hi = GRIDS[tag]
+        g = build_grid(n, m, k, lo, hi)
+        params = ModelParams(N=n, m_rad=m, m_ang=k, p2_min=lo, p2_max=hi)
+        states = {
+            "init": (np.ones(n), np.full(n, 0.3)),
+            "random": (rng.uniform(0.8, 2.0, n), rng.uniform(0.0, 1.5, n)),
+        }
+        for sname, (a, b) in states.items():
+            for pname, p in (("defaults", params),
+                             ("m0z1", ModelParams(N=n, m_rad=m, m_ang=k, p2_min=lo, p2_max=hi,
+                                                  m0=0.005, z1=1.3, D=0.93, omega=0.5))):
+                an, bn = iterate_once(g, a, b, p, VARIANTS["indexed-seq"])
+                an2, bn2 = iterate_once(g, a, b, p, VARIANTS["search-seq"])
+                assert np.array_equal(an, an2) and np.array_equal(bn, bn2)
+                cases.append((f"{tag}_{sname}_{pname}", tag, p, a, b, an, bn))
+    out = {}
+    for name, tag, p, a, b, an, bn in cases:
+        out[f"{name}__grid"] = np.array(tag)
+        out[f"{name}__params"] = np.array([p.D, p.omega, p.m0, p.z1, p.interaction_coeff])
+        out[f"{name}__a"] = a
+        out[f"{name}__b"] = b
+        out[f"{name}__a_out"] = an
+        out[f"{name}__b_out"] = bn
+    save("sweeps.npz", names=np.array([c[0] for c in cases]),
+         call="iterate_once(grid, a, b, params, VARIANTS['indexed-seq']) (== search-seq bitwise)",
+         **out)
+
+
+def _solve_to_npz(name, n, m, k, params, threads, b0):
+    g = build_grid(n, m, k, params.p2_min, params.p2_max)
+    t0 = time.perf_counter()
+    sol = solve(params, VARIANTS["indexed-par"].with_threads(threads), grid=g, b0=b0)
+    wall = time.perf_counter() - t0
+    hist = np.array([[r.iteration, r.max_delta_a, r.max_delta_b, *r.probe_a, *r.probe_b]
+                     for r in sol.history])
+    save(name, A=sol.A, B=sol.B, iterations=np.array(sol.iterations),
+         converged=np.array(sol.converged), history=hist,
+         params=np.array([params.D, params.omega, params.m0, params.z1, params.xi,
+                          params.relaxation, params.max_iterations, params.interaction_coeff]),
+         probes_log10p=np.array(sol.probes_log10p), b0=np.ones(n) if b0 is None else b0, wall_s=np.array(wall),
+         threads=np.array(threads),
+         call=f"solve(ModelParams(N={n},m_rad={m},m_ang={k},xi={params.xi},"
+              f"max_iterations={params.max_iterations},relaxation={params.relaxation}), "
+              f"VARIANTS['indexed-par'].with_threads({threads}), grid=build_grid(...), b0=b0)")
+    print(name, "iterations", sol.iterations, "converged", sol.converged, f"{wall:.1f}s")
+
+
+def make_solve_c0(threads):
+    p = ModelParams(N=128, m_rad=128, m_ang=64, xi=1e-10, max_iterations=20000)
+    _solve_to_npz("solve_c0.npz", 128, 128, 64, p, threads, np.full(128, 0.3))
+
+
+def make_solve_default(threads):
+    p = ModelParams()
+    _solve_to_npz("solve_default.npz", p.N, p.m_rad, p.m_ang, p, threads, None)
+
+
+def make_solve_c2k10(threads):
+    p = ModelParams(N=1024, m_rad=1024, m_ang=256, xi=1e-10, max_iterations=10)
+    _solve_to_npz("solve_c2k10.npz", 1024, 1024, 256, p, threads, np.full(1024, 0.3))
+
+
+def make_solve_sub256(threads):
+    p = ModelParams(N=256, m_rad=256, m_ang=256, xi=1e-10, max_iterations=2000, relaxation=0.5)
+    _solve_to_npz("solve_sub256.npz", 256, 256, 256, p, threads, np.full(256, 0.3))
+
+
+def make_interp():
+    x = np.logspace(-4, 4, 512)
+    v = 1.0 / (1.0 + x) + 0.1 * np.log1p(x)
+    rng = np.random.default_rng(0)
+    q = np.exp(rng.uniform(np.log(1e-4), np.log(1e4), 2 ** 16))
+    # edge queries: below, at every knot, just above/below knots, at/above the end
+    edge = np.concatenate([[0.0, 1e-5, x[0], np.nextafter(x[0], 0), x[-1],
+                            np.nextafter(x[-1], np.inf), 1e5, np.inf, -1.0],
+                           x, np.nextafter(x, 0), np.nextafter(x, np.inf)])
+    allq = np.concatenate([q, edge])
+    vals = interp_search_many(x, v, allq)
+    idx = np.array([_bracket_search(x, float(t)) for t in allq], dtype=np.int64)
+    cnt = dsegap.ComparisonCounter()
+    interp_search_many(x, v, allq, counter=cnt)
+    # a small non-uniform table too
+    x2 = np.array([0.5, 1.0, 1.5, 4.0, 4.5, 10.0])
+    v2 = np.array([3.0, -1.0, 2.0, 2.0, 7.0, 0.25])
+    q2 = np.concatenate([np.linspace(0.0, 11.0, 1001), x2])
+    vals2 = interp_search_many(x2, v2, q2)
+    idx2 = np.array([_bracket_search(x2, float(t)) for t in q2], dtype=np.int64)
+    save("interp_c1.npz", x=x, v=v, q=allq, n_random=np.array(2 ** 16), values=vals, idx=idx,
+         comparisons=np.array(cnt.count), x2=x2, v2=v2, q2=q2, values2=vals2, idx2=idx2,
+         call="interp_search_many(x, v, q); _bracket_search(x, q) per query")
+
+
+def make_errors():
+    out = {}
+    names = []
+    g = build_grid(20, 16, 8, 1e-6, 1e4)
+    p = ModelParams(N=20, m_rad=16, m_ang=8)
+    cases = {
+        "nan_a7": (lambda a, b: (a.__setitem__(7, np.nan), b)),
+        "inf_b3": (lambda a, b: (a, b.__setitem__(3, np.inf))),
+        "zero_den": None,
+    }
+    for name in cases:
+        a = np.ones(20)
+        b = np.full(20, 0.3)
+        if name == "nan_a7":
+            a[7] = np.nan
+        elif name == "inf_b3":
+            b[3] = np.inf
+        else:  # A = B = 0 at every node -> den = 0 -> 0/0 in core
+            a[:] = 0.0
+            b[:] = 0.0
+        try:
+            iterate_once(g, a, b, p, VARIANTS["indexed-seq"])
+            loc = (-9, -9, -9)
+        except NumericalFailureError as exc:
+            loc = (exc.row, exc.radial, exc.angular)
+        names.append(name)
+        out[f"{name}__a"] = a
+        out[f"{name}__b"] = b
+        out[f"{name}__loc"] = np.array(loc)
+    save("errors.npz", names=np.array(names), grid=np.array("small"), **out)
+
+
+def make_sweeps_libm():
+    """Same inputs as make_sweeps, but the reference's np.exp is routed through
+    glibc exp (math.exp) for the duration: pins the oracle's operation order
+    BITWISE (the oracle uses glibc exp; numpy's SIMD exp differs by <=1 ulp)."""
+    import math
+    grids = {t: build_grid(*GRIDS[t]) for t in ("c0", "default", "small", "ragged", "tiny")}
+    src = np.load(os.path.join(HERE, "sweeps.npz"))
+    real_exp = np.exp
+    libm_exp = np.frompyfunc(math.exp, 1, 1)
+    np.exp = lambda x: libm_exp(x).astype(np.float64)
+    try:
+        out = {}
+        for name in src["names"]:
+            tag = str(src[f"{name}__grid"])
+            D, om, m0, z1, _ = src[f"{name}__params"]
+            n, m, k, lo, hi = GRIDS[tag]
+            p = ModelParams(N=n, m_rad=m, m_ang=k, p2_min=lo, p2_max=hi, D=D, omega=om, m0=m0, z1=z1)
+            an, bn = iterate_once(grids[tag], src[f"{name}__a"], src[f"{name}__b"], p,
+                                  VARIANTS["indexed-seq"])
+            out[f"{name}__a_out"] = an
+            out[f"{name}__b_out"] = bn
+    finally:
+        np.exp = real_exp
+    save("sweeps_libm.npz", names=src["names"],
+         call="iterate_once(...) with numpy.exp -> math.exp (glibc) during the sweep", **out)
+
+
+JOBS = {
+    "sweeps_libm": lambda t: make_sweeps_libm(),
+    "grids": lambda t: make_grids(),
+    "sweeps": lambda t: make_sweeps(),
+    "interp": lambda t: make_interp(),
+    "errors": lambda t: make_errors(),
+    "solve_default": make_solve_default,
+    "solve_c0": make_solve_c0,
+    "solve_c2k10": make_solve_c2k10,
+    "solve_sub256": make_solve_sub256,
+}
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", nargs="*", default=list(JOBS))
+    ap.add_argument("--threads", type=int, default=os.cpu_count())
+    args = ap.parse_args()
+    for name in args.only:
+        JOBS[name](args.threads)

@@ -1,0 +1,87 @@
+"""CPU, world_size 2 over gloo: the row-sharded loop (partition, all-gather,
+reassembly, relaxation, max-norm deltas, history) equals the unsharded loop
+bitwise.  The per-row map is a synthetic Jacobi contraction (a test double
+for the GPU sweep): this tests the host logic of distributed.py, the GPU
+sweep's own row-sharding invariance is tests/test_gpu_sweep.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2012_03667_b200.distributed import ShardedLoop, owned_rows
+
+N = 37
+
+
+def jacobi_map(a, b):
+    """a'_i, b'_i depend on the whole previous iterate (like the qDSE sweep)."""
+    a_next = 1.0 + 0.4 * np.sin(np.roll(a, 1)) + 0.1 * b + 0.01 * np.mean(a)
+    b_next = 0.3 + 0.2 * np.cos(np.roll(b, 3)) + 0.1 * a
+    return a_next, b_next
+
+
+def probe(a, b):
+    x = np.linspace(1.0, 2.0, N)
+    return np.interp([1.25, 1.7], x, a), np.interp([1.25, 1.7], x, b)
+
+
+def _run(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rows = owned_rows(N, rank, world)
+
+    def sweep_rows(a, b):
+        an, bn = jacobi_map(a, b)
+        return an[rows], bn[rows]
+
+    def gather(buf):
+        parts = [torch.empty(buf.shape, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(np.ascontiguousarray(buf)))
+        return np.stack([t.numpy() for t in parts])
+
+    loop = ShardedLoop(N, rank, world, sweep_rows, gather, probe)
+    res = loop.run(np.ones(N), np.full(N, 0.3), 1e-12, 200, 0.5)
+    q.put((rank, res))
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _single():
+    loop = ShardedLoop(N, 0, 1, lambda a, b: jacobi_map(a, b), lambda buf: buf[None], probe)
+    return loop.run(np.ones(N), np.full(N, 0.3), 1e-12, 200, 0.5)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_loop_matches_single_process(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a1, b1, n1, c1, h1 = _single()
+    assert c1 and n1 < 200
+    for r in range(world):
+        a, b, n, c, h = out[r]
+        assert n == n1 and c == c1
+        assert np.array_equal(a, a1) and np.array_equal(b, b1)
+        assert np.array_equal(h, h1, equal_nan=True)
+
+
+def test_owned_rows_partition():
+    for world in (1, 2, 3, 8):
+        allrows = np.sort(np.concatenate([owned_rows(1024, r, world) for r in range(world)]))
+        assert np.array_equal(allrows, np.arange(1024))

@@ -1,0 +1,87 @@
+"""GPU parity of the on-device successive-approximation loop (solve).
+
+North-star bar: converged A, B within 1e-9 relative (hybrid measure, SURVEY
+§8c) of the reference's own CPU solve, and EXACTLY the same iteration count.
+"""
+import numpy as np
+import pytest
+
+import paper_2012_03667_b200 as p
+from conftest import golden, golden_grid, hybrid_rel, params_ns
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(fname, tag, variant):
+    z = golden(fname)
+    D, om, m0, z1, xi, relax, cap, c = z["params"]
+    prm = params_ns(D=D, omega=om, m0=m0, z1=z1, xi=xi, relaxation=relax, max_iterations=int(cap), coeff=c)
+    g = golden_grid(tag)
+    b0 = z["b0"] if z["b0"].shape == (g.n_ext,) else None
+    sol = p.solve(prm, variant, grid=g, probes_log10p=tuple(z["probes_log10p"]), b0=b0)
+    return z, sol
+
+
+def _hist(sol):
+    return np.array([[r.iteration, r.max_delta_a, r.max_delta_b, *r.probe_a, *r.probe_b] for r in sol.history])
+
+
+@pytest.mark.parametrize("vname", ["indexed-gpu", "search-gpu", "indexed-gpu-fast"])
+def test_solve_default_config(vname):
+    z, sol = _run("solve_default.npz", "default", p.VARIANTS[vname])
+    assert sol.iterations == int(z["iterations"]) and sol.converged == bool(z["converged"])
+    assert hybrid_rel(sol.A, z["A"]) <= 1e-11 and hybrid_rel(sol.B, z["B"]) <= 1e-11
+    h = _hist(sol)
+    assert h.shape == z["history"].shape
+    assert np.isnan(h[0, 1]) and np.isnan(h[0, 2])
+    np.testing.assert_allclose(h[1:, 1:3], z["history"][1:, 1:3], rtol=1e-6)
+    np.testing.assert_allclose(h[:, 3:], z["history"][:, 3:], rtol=1e-11)
+
+
+@pytest.mark.parametrize("vname", ["indexed-gpu", "indexed-gpu-fast"])
+def test_solve_config0_exact_iteration_count(vname):
+    """Config 0 (128/128/64, xi=1e-10, b0=0.3): the reference converges in 2923 sweeps."""
+    z, sol = _run("solve_c0.npz", "c0", p.VARIANTS[vname])
+    assert sol.converged and sol.iterations == int(z["iterations"]) == 2923
+    assert hybrid_rel(sol.A, z["A"]) <= 1e-9 and hybrid_rel(sol.B, z["B"]) <= 1e-9
+    h = _hist(sol)
+    assert h.shape == z["history"].shape
+
+
+@pytest.mark.parametrize("vname", ["indexed-gpu", "indexed-gpu-fast"])
+def test_solve_config2_first_10_sweeps(vname):
+    """Config 2 (1024/1024/256) does not converge in the reference:
+    parity = first 10 sweeps + converged=False at the same cap."""
+    z, sol = _run("solve_c2k10.npz", "c2", p.VARIANTS[vname])
+    assert sol.iterations == 10 and not sol.converged and not bool(z["converged"])
+    assert hybrid_rel(sol.A, z["A"]) <= 1e-11 and hybrid_rel(sol.B, z["B"]) <= 1e-11
+    np.testing.assert_allclose(_hist(sol)[1:, 1:3], z["history"][1:, 1:3], rtol=1e-6)
+
+
+@pytest.mark.parametrize("vname", ["indexed-gpu", "indexed-gpu-fast"])
+def test_solve_large_substitute_relaxation(vname):
+    """N=M=K=256 at relaxation 0.5: the reference converges in 421 iterations."""
+    z, sol = _run("solve_sub256.npz", "sub256", p.VARIANTS[vname])
+    assert sol.converged and sol.iterations == int(z["iterations"])
+    assert hybrid_rel(sol.A, z["A"]) <= 1e-9 and hybrid_rel(sol.B, z["B"]) <= 1e-9
+
+
+def test_solve_cap_and_warm_start():
+    g = golden_grid("default")
+    prm = params_ns(xi=1e-14, max_iterations=3)
+    sol = p.solve(prm, p.VARIANTS["indexed-gpu"], grid=g)
+    assert sol.iterations == 3 and not sol.converged and len(sol.history) == 4
+    # warm start from the 3-iteration state continues the same trajectory
+    a, b = np.ones(g.n_ext), np.ones(g.n_ext)
+    for _ in range(3):
+        a, b = p.iterate_once(g, a, b, prm, p.VARIANTS["indexed-gpu"])
+    assert np.array_equal(a, sol.A) and np.array_equal(b, sol.B)
+
+
+def test_solve_numerical_failure_raises():
+    g = golden_grid("small")
+    a0 = np.ones(g.n_ext)
+    a0[5] = np.inf
+    with pytest.raises(p.NumericalFailureError) as ei:
+        p.solve(params_ns(xi=1e-3, max_iterations=5), p.VARIANTS["indexed-gpu"], grid=g, a0=a0)
+    assert ei.value.iteration == 1 and ei.value.row is not None

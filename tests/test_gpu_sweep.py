@@ -1,0 +1,108 @@
+"""GPU parity of one Jacobi sweep (iterate_once) through the C ABI.
+
+Oracle: golden vectors from the reference itself (tests/golden/sweeps.npz)
+and the C restatement (oracle/).  Tolerances (SURVEY.md §8c hybrid measure):
+  exact arithmetic : <= 1e-13 (only the device exp differs, <= 1 ulp)
+  fast arithmetic  : <= 1e-12
+The reference's own bound for iterate_once vs its brute oracle is 1e-11
+(test_solver.py:83-91).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2012_03667_b200 as p
+from conftest import golden, golden_grid, hybrid_rel, params_ns
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"exact": 1e-13, "fast": 1e-12}
+VAR = {"exact": p.VARIANTS["indexed-gpu"], "fast": p.VARIANTS["indexed-gpu-fast"]}
+
+
+def _params(S, name):
+    D, om, m0, z1, c = S[f"{name}__params"]
+    return params_ns(D=D, omega=om, m0=m0, z1=z1, coeff=c)
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_sweep_vs_reference_golden(arith):
+    S = golden("sweeps.npz")
+    for name in S["names"]:
+        g = golden_grid(str(S[f"{name}__grid"]))
+        prm = _params(S, name)
+        a, b = p.iterate_once(g, S[f"{name}__a"], S[f"{name}__b"], prm, VAR[arith])
+        ea, eb = hybrid_rel(a, S[f"{name}__a_out"]), hybrid_rel(b, S[f"{name}__b_out"])
+        assert ea <= TOL[arith] and eb <= TOL[arith], (name, ea, eb)
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+@pytest.mark.parametrize("tag", ["c0", "ragged", "sub256", "c2"])
+def test_sweep_vs_oracle_random_states(arith, tag):
+    g = golden_grid(tag)
+    rng = np.random.default_rng(7)
+    prm = params_ns(m0=0.003)
+    for _ in range(2):
+        a = rng.uniform(0.9, 2.5, g.n_ext)
+        b = rng.uniform(0.0, 1.6, g.n_ext)
+        ra, rb = oracle.sweep(g, a, b, prm, strategy=1, threads=oracle.max_threads())
+        ga, gb = p.iterate_once(g, a, b, prm, VAR[arith])
+        assert hybrid_rel(ga, ra) <= TOL[arith] and hybrid_rel(gb, rb) <= TOL[arith]
+
+
+def test_search_and_indexed_bitwise_equal_and_deterministic():
+    g = golden_grid("c0")
+    rng = np.random.default_rng(1)
+    a, b = rng.uniform(1, 2, g.n_ext), rng.uniform(0, 1, g.n_ext)
+    prm = params_ns()
+    r1 = p.iterate_once(g, a, b, prm, p.VARIANTS["indexed-gpu"])
+    r2 = p.iterate_once(g, a, b, prm, p.VARIANTS["search-gpu"])
+    r3 = p.iterate_once(g, a, b, prm, p.VARIANTS["indexed-gpu"])
+    for x, y in ((r1, r2), (r1, r3)):
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_row_sharded_sweepers_assemble_bitwise(world):
+    """Rows owned by rank r of W (r, r+W, ...) reproduce the full sweep bitwise:
+    a row's reduction never depends on which sweeper/GPU computes it."""
+    g = golden_grid("default")
+    rng = np.random.default_rng(2)
+    a, b = rng.uniform(1, 2, g.n_ext), rng.uniform(0, 1, g.n_ext)
+    prm = params_ns()
+    full = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX).sweep(a, b)
+    ao, bo = np.full(g.n_ext, np.nan), np.full(g.n_ext, np.nan)
+    for r in range(world):
+        sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, rows=(r, world))
+        x, y = sw.sweep(a, b)
+        ao[r::world], bo[r::world] = x[r::world], y[r::world]
+        sw.close()
+    assert np.array_equal(ao, full[0]) and np.array_equal(bo, full[1])
+
+
+def test_free_theory_and_chiral_limit():
+    g = golden_grid("small")
+    free = params_ns(D=0.0, m0=0.01)
+    a, b = p.iterate_once(g, np.full(g.n_ext, 1.7), np.full(g.n_ext, 0.2), free, p.VARIANTS["indexed-gpu"])
+    assert np.all(a == 1.0) and np.all(b == 0.01)
+    a, b = np.full(g.n_ext, 1.3), np.zeros(g.n_ext)
+    for _ in range(10):
+        a, b = p.iterate_once(g, a, b, params_ns(), p.VARIANTS["indexed-gpu"])
+        assert np.all(b == 0.0)
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_numerical_failure_location(arith):
+    E = golden("errors.npz")
+    g = golden_grid("small")
+    for name in E["names"]:
+        with pytest.raises(p.NumericalFailureError) as ei:
+            p.iterate_once(g, E[f"{name}__a"], E[f"{name}__b"], params_ns(), VAR[arith])
+        exc = ei.value
+        assert (exc.row, exc.radial, exc.angular) == tuple(int(v) for v in E[f"{name}__loc"]), name
+
+
+def test_shape_validation():
+    g = golden_grid("small")
+    with pytest.raises(p.ParameterError):
+        p.iterate_once(g, np.ones(3), np.ones(g.n_ext), params_ns(), p.VARIANTS["indexed-gpu"])
