@@ -76,6 +76,8 @@ _PROTOS = [
     ("dse_solve_resume", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
     ("dse_sweeper_stats", ctypes.c_int, [ctypes.c_void_p, i64p, i64p, i64p, i32p, i64p]),
     ("dse_fp64_peak", ctypes.c_int, [ctypes.c_int, f64p, ctypes.POINTER(DseErr)]),
+    ("dse_debug_pairwise_sum", ctypes.c_int, [ctypes.c_int, f64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_int64, f64p, f64p, ctypes.POINTER(DseErr)]),
     ("dse_launch_count", ctypes.c_int64, []),
 ]
 
@@ -136,3 +138,17 @@ def as_i64(a):
 
 def launch_count() -> int:
     return int(load().dse_launch_count())
+
+
+def debug_pairwise_sum(vals, chunk_leaves: int = 0, device: int = 0):
+    """Test hook (dse_debug_pairwise_sum): the production kernel's reduction of
+    vals[rows, m, k] per row; returns (sum(v), sum(-2 v)) per row."""
+    import ctypes as _ct
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    rows, m, k = v.shape
+    oa, ob = np.empty(rows), np.empty(rows)
+    err = DseErr()
+    rc = load().dse_debug_pairwise_sum(device, v.ctypes.data_as(f64p), rows, m, k, int(chunk_leaves),
+                                       oa.ctypes.data_as(f64p), ob.ctypes.data_as(f64p), _ct.byref(err))
+    raise_for(rc, err)
+    return oa, ob
