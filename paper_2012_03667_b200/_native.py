@@ -14,7 +14,7 @@ import numpy as np
 from .errors import ExecutionEnvironmentError, NumericalFailureError, ParameterError
 
 LIB_NAME = "libdse_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("DSE_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 DSE_OK, DSE_EPARAM, DSE_ENUMERIC, DSE_EENV = 0, 1, 2, 3
 INTERP_SEARCH, INTERP_INDEXED = 0, 1
@@ -97,6 +97,8 @@ def load(path: str = LIB_PATH):
     except OSError as exc:
         raise ExecutionEnvironmentError(f"cannot load {path}: {exc}") from exc
     for name, res, args in _PROTOS:
+        if not hasattr(lib, name) and os.environ.get("DSE_LIB"):
+            continue  # an older library under A/B test
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
