@@ -361,7 +361,7 @@ def run_ours_distributed(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--arith", choices=["exact", "fast"], default=os.environ.get("DSE_BENCH_ARITH", "exact"))
