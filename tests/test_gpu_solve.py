@@ -26,7 +26,7 @@ def _hist(sol):
     return np.array([[r.iteration, r.max_delta_a, r.max_delta_b, *r.probe_a, *r.probe_b] for r in sol.history])
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu", "search-gpu", "indexed-gpu-fast"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "search-gpu-exact", "indexed-gpu"])
 def test_solve_default_config(vname):
     z, sol = _run("solve_default.npz", "default", p.VARIANTS[vname])
     assert sol.iterations == int(z["iterations"]) and sol.converged == bool(z["converged"])
@@ -38,7 +38,7 @@ def test_solve_default_config(vname):
     np.testing.assert_allclose(h[:, 3:], z["history"][:, 3:], rtol=1e-11)
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu", "indexed-gpu-fast"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu"])
 def test_solve_config0_exact_iteration_count(vname):
     """Config 0 (128/128/64, xi=1e-10, b0=0.3): the reference converges in 2923 sweeps."""
     z, sol = _run("solve_c0.npz", "c0", p.VARIANTS[vname])
@@ -48,7 +48,7 @@ def test_solve_config0_exact_iteration_count(vname):
     assert h.shape == z["history"].shape
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu", "indexed-gpu-fast"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu"])
 def test_solve_config2_first_10_sweeps(vname):
     """Config 2 (1024/1024/256) does not converge in the reference:
     parity = first 10 sweeps + converged=False at the same cap."""
@@ -58,7 +58,7 @@ def test_solve_config2_first_10_sweeps(vname):
     np.testing.assert_allclose(_hist(sol)[1:, 1:3], z["history"][1:, 1:3], rtol=1e-6)
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu", "indexed-gpu-fast"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu"])
 def test_solve_large_substitute_relaxation(vname):
     """N=M=K=256 at relaxation 0.5: the reference converges in 421 iterations."""
     z, sol = _run("solve_sub256.npz", "sub256", p.VARIANTS[vname])
@@ -69,12 +69,12 @@ def test_solve_large_substitute_relaxation(vname):
 def test_solve_cap_and_warm_start():
     g = golden_grid("default")
     prm = params_ns(xi=1e-14, max_iterations=3)
-    sol = p.solve(prm, p.VARIANTS["indexed-gpu"], grid=g)
+    sol = p.solve(prm, p.VARIANTS["indexed-gpu-exact"], grid=g)
     assert sol.iterations == 3 and not sol.converged and len(sol.history) == 4
     # warm start from the 3-iteration state continues the same trajectory
     a, b = np.ones(g.n_ext), np.ones(g.n_ext)
     for _ in range(3):
-        a, b = p.iterate_once(g, a, b, prm, p.VARIANTS["indexed-gpu"])
+        a, b = p.iterate_once(g, a, b, prm, p.VARIANTS["indexed-gpu-exact"])
     assert np.array_equal(a, sol.A) and np.array_equal(b, sol.B)
 
 
@@ -83,5 +83,5 @@ def test_solve_numerical_failure_raises():
     a0 = np.ones(g.n_ext)
     a0[5] = np.inf
     with pytest.raises(p.NumericalFailureError) as ei:
-        p.solve(params_ns(xi=1e-3, max_iterations=5), p.VARIANTS["indexed-gpu"], grid=g, a0=a0)
+        p.solve(params_ns(xi=1e-3, max_iterations=5), p.VARIANTS["indexed-gpu-exact"], grid=g, a0=a0)
     assert ei.value.iteration == 1 and ei.value.row is not None

@@ -17,7 +17,7 @@ from conftest import golden, golden_grid, hybrid_rel, params_ns
 pytestmark = pytest.mark.gpu
 
 TOL = {"exact": 1e-13, "fast": 1e-12}
-VAR = {"exact": p.VARIANTS["indexed-gpu"], "fast": p.VARIANTS["indexed-gpu-fast"]}
+VAR = {"exact": p.VARIANTS["indexed-gpu-exact"], "fast": p.VARIANTS["indexed-gpu"]}
 
 
 def _params(S, name):
@@ -55,9 +55,9 @@ def test_search_and_indexed_bitwise_equal_and_deterministic():
     rng = np.random.default_rng(1)
     a, b = rng.uniform(1, 2, g.n_ext), rng.uniform(0, 1, g.n_ext)
     prm = params_ns()
-    r1 = p.iterate_once(g, a, b, prm, p.VARIANTS["indexed-gpu"])
-    r2 = p.iterate_once(g, a, b, prm, p.VARIANTS["search-gpu"])
-    r3 = p.iterate_once(g, a, b, prm, p.VARIANTS["indexed-gpu"])
+    r1 = p.iterate_once(g, a, b, prm, p.VARIANTS["indexed-gpu-exact"])
+    r2 = p.iterate_once(g, a, b, prm, p.VARIANTS["search-gpu-exact"])
+    r3 = p.iterate_once(g, a, b, prm, p.VARIANTS["indexed-gpu-exact"])
     for x, y in ((r1, r2), (r1, r3)):
         assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
 
@@ -83,11 +83,11 @@ def test_row_sharded_sweepers_assemble_bitwise(world):
 def test_free_theory_and_chiral_limit():
     g = golden_grid("small")
     free = params_ns(D=0.0, m0=0.01)
-    a, b = p.iterate_once(g, np.full(g.n_ext, 1.7), np.full(g.n_ext, 0.2), free, p.VARIANTS["indexed-gpu"])
+    a, b = p.iterate_once(g, np.full(g.n_ext, 1.7), np.full(g.n_ext, 0.2), free, p.VARIANTS["indexed-gpu-exact"])
     assert np.all(a == 1.0) and np.all(b == 0.01)
     a, b = np.full(g.n_ext, 1.3), np.zeros(g.n_ext)
     for _ in range(10):
-        a, b = p.iterate_once(g, a, b, params_ns(), p.VARIANTS["indexed-gpu"])
+        a, b = p.iterate_once(g, a, b, params_ns(), p.VARIANTS["indexed-gpu-exact"])
         assert np.all(b == 0.0)
 
 
@@ -105,4 +105,4 @@ def test_numerical_failure_location(arith):
 def test_shape_validation():
     g = golden_grid("small")
     with pytest.raises(p.ParameterError):
-        p.iterate_once(g, np.ones(3), np.ones(g.n_ext), params_ns(), p.VARIANTS["indexed-gpu"])
+        p.iterate_once(g, np.ones(3), np.ones(g.n_ext), params_ns(), p.VARIANTS["indexed-gpu-exact"])
