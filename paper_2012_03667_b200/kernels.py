@@ -61,8 +61,8 @@ def row_rhs(p2: float, a_p: float, b_p: float, a_q, b_q, grid, params: ModelPara
             row: int | None = None) -> tuple[float, float]:
     """(A', B') for one external momentum (kernels.py:178-226), on the GPU.
 
-    Runs a one-row sweep: the external grid is the single node p2 and the
-    dressing values at the internal nodes are the given a_q, b_q.
+    One-row sweep through the C ABI (dse_row_rhs) in the exact arithmetic,
+    with the caller's dressing values a_q, b_q at the internal nodes.
     """
     from .solver import _row_rhs_gpu
     return _row_rhs_gpu(p2, a_p, b_p, a_q, b_q, grid, params, row)

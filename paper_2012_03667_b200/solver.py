@@ -352,6 +352,25 @@ def solve(params: ModelParams, variant: AlgorithmVariant, grid: MomentumGrid | N
                               params=params, probes_log10p=tuple(probes_log10p))
 
 
-def _row_rhs_gpu(p2, a_p, b_p, a_q, b_q, grid, params, row):
-    raise NotImplementedError("row_rhs on an arbitrary (a_q, b_q) is served by the sweep; "
-                              "use iterate_once for full rows")
+def _row_rhs_gpu(p2, a_p, b_p, a_q, b_q, grid, params, row, arith: Arithmetic = Arithmetic.EXACT):
+    """row_rhs (kernels.py:178-226) through dse_row_rhs: one external row with
+    the caller's a_q, b_q (exact arithmetic by default, like the reference)."""
+    lib = nat.load()
+    keep = [nat.as_f64(grid.p2_ext), nat.as_f64(grid.q2_int), nat.as_f64(grid.sqrt_q2_int),
+            nat.as_f64(grid.radial_measure), nat.as_i64(grid.bracket_idx), nat.as_f64(grid.z_nodes),
+            nat.as_f64(grid.z_weights)]
+    g = nat.DseGrid(*(p for _, p in keep), grid.n_ext, grid.m_rad, grid.m_ang)
+    aq, paq = nat.as_f64(a_q)
+    bq, pbq = nat.as_f64(b_q)
+    if aq.shape != (grid.m_rad,) or bq.shape != (grid.m_rad,):
+        raise ParameterError("a_q and b_q must match the internal grid size")
+    prm = _c_params(params)
+    oa, ob = ctypes.c_double(), ctypes.c_double()
+    err = nat.DseErr()
+    rc = lib.dse_row_rhs(ctypes.byref(g), ctypes.byref(prm), nat.ARITH_FAST if arith is Arithmetic.FAST else
+                         nat.ARITH_EXACT, _device(), float(p2), float(a_p), float(b_p), paq, pbq,
+                         -1 if row is None else int(row), ctypes.byref(oa), ctypes.byref(ob), ctypes.byref(err))
+    if rc == nat.DSE_ENUMERIC and row is None:
+        err.row = -1
+    nat.raise_for(rc, err)
+    return oa.value, ob.value

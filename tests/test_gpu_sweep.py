@@ -106,3 +106,29 @@ def test_shape_validation():
     g = golden_grid("small")
     with pytest.raises(p.ParameterError):
         p.iterate_once(g, np.ones(3), np.ones(g.n_ext), params_ns(), p.VARIANTS["indexed-gpu-exact"])
+
+
+def test_row_rhs_matches_sweep_and_reference_formula():
+    """row_rhs (kernels.py:178) with a_q, b_q from the internal-node
+    interpolation equals that row of the full sweep bitwise."""
+    S = golden("sweeps.npz")
+    name = "c0_random_m0z1"
+    g = golden_grid("c0")
+    prm = _params(S, name)
+    a, b = S[f"{name}__a"], S[f"{name}__b"]
+    aq, bq = p.interp_indexed_many(g, a), p.interp_indexed_many(g, b)
+    full = p.iterate_once(g, a, b, prm, p.VARIANTS["indexed-gpu-exact"])
+    for i in (0, 17, 64, 127):
+        ra, rb = p.row_rhs(g.p2_ext[i], a[i], b[i], aq, bq, g, prm, row=i)
+        assert ra == full[0][i] and rb == full[1][i]
+        assert abs(ra - S[f"{name}__a_out"][i]) <= 1e-13 * abs(S[f"{name}__a_out"][i])
+
+
+def test_row_rhs_nonfinite_location():
+    g = golden_grid("small")
+    aq = np.ones(g.m_rad)
+    bq = np.full(g.m_rad, 0.3)
+    bq[4] = np.nan
+    with pytest.raises(p.NumericalFailureError) as ei:
+        p.row_rhs(g.p2_ext[3], 1.0, 0.3, aq, bq, g, params_ns(), row=3)
+    assert (ei.value.row, ei.value.radial, ei.value.angular) == (3, 4, 0)
