@@ -167,7 +167,7 @@ def run_ours(args):
     from paper_2012_03667_b200 import _native as nat
 
     rank, world, local = _env_rank()
-    if world > 1:
+    if world > 1 or os.environ.get("DSE_FORCE_DIST") == "1":
         return run_ours_distributed(args)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

@@ -1,0 +1,56 @@
+"""GPU: the NCCL row-sharded solve (distributed.py) on one rank equals the
+single-GPU solve bitwise (real NCCL all-gather, real sharded sweeper).  The
+multi-rank host logic is covered by tests/test_distributed.py (gloo)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2012_03667_b200 as p
+from conftest import golden, golden_grid, params_ns
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def nccl_world1():
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0", WORLD_SIZE="1",
+                      LOCAL_RANK="0")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    yield dist
+    dist.destroy_process_group()
+
+
+def test_sharded_solve_world1_bitwise(nccl_world1):
+    z = golden("solve_default.npz")
+    g = golden_grid("default")
+    prm = params_ns(xi=0.005, max_iterations=500)
+    ref = p.solve(prm, p.VARIANTS["indexed-gpu"], grid=g)
+    sol = p.solve(prm, p.VARIANTS["indexed-gpu"].with_threads(1), grid=g)  # threads=1 -> single GPU
+    from paper_2012_03667_b200.distributed import solve_sharded
+    a, b, n, conv, hist = solve_sharded(g, prm, p.VARIANTS["indexed-gpu"].with_threads(1), np.ones(g.n_ext),
+                                        np.ones(g.n_ext), tuple(10.0 ** (2.0 * lp) for lp in (-2.5, 0.0)))
+    assert n == ref.iterations == sol.iterations == int(z["iterations"]) and conv
+    assert np.array_equal(a, ref.A) and np.array_equal(b, ref.B)
+    h_ref = np.array([[r.iteration, r.max_delta_a, r.max_delta_b, *r.probe_a, *r.probe_b] for r in ref.history])
+    assert np.array_equal(hist, h_ref, equal_nan=True)
+
+
+def test_sharded_sweep_world1_bitwise(nccl_world1):
+    g = golden_grid("c0")
+    rng = np.random.default_rng(5)
+    a, b = rng.uniform(1, 2, g.n_ext), rng.uniform(0, 1, g.n_ext)
+    from paper_2012_03667_b200.distributed import iterate_once_sharded
+    x = iterate_once_sharded(g, a, b, params_ns(), p.VARIANTS["indexed-gpu"].with_threads(1))
+    y = p.iterate_once(g, a, b, params_ns(), p.VARIANTS["indexed-gpu"])
+    assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
