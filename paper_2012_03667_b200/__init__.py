@@ -10,6 +10,7 @@ from .errors import (ConsistencyError, DegenerateMomentumError, ExecutionEnviron
                      GridConstructionError, KinematicSingularityError, NumericalFailureError,
                      ParameterError)
 from .grid import MomentumGrid, build_grid, merge_bracket_indices
+from .harness import BenchReport, BenchRow, format_table, run_bench
 from .interpolation import (ComparisonCounter, InterpStrategy, interp_indexed, interp_indexed_many,
                             interp_linear_batch, interp_search, interp_search_many)
 from .iteration import successive_approximation
@@ -24,6 +25,7 @@ __all__ = [
     "ConsistencyError", "DegenerateMomentumError", "ExecutionEnvironmentError", "GridConstructionError",
     "KinematicSingularityError", "NumericalFailureError", "ParameterError",
     "MomentumGrid", "build_grid", "merge_bracket_indices",
+    "BenchReport", "BenchRow", "format_table", "run_bench",
     "ComparisonCounter", "InterpStrategy", "interp_indexed", "interp_indexed_many", "interp_linear_batch",
     "interp_search", "interp_search_many",
     "successive_approximation", "ModelParams", "row_rhs",
