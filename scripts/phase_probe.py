@@ -17,12 +17,15 @@ for arith in (p.Arithmetic.FAST,):
         sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, arith)
         sw.solve(np.ones(n), np.full(n, 0.3))
         sw.solve(np.ones(n), np.full(n, 0.3))
-        out = np.zeros((it, 5))
+        out = np.zeros((it, 9))
         lib = ctypes.CDLL(os.environ["DSE_LIB"])
         lib.dse_debug_phase_times.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int64]
         assert lib.dse_debug_phase_times(out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), it) == 0
-        d = np.diff(out, axis=1)[5:]  # skip the first iterations
+        o = out[5:]
         total = (out[6:, 0] - out[5:-1, 0])
-        print(f"N={n} M={m} K={k} {arith.value}: per iteration {np.median(total)/1e3:.2f} us; "
-              f"prologue {np.median(d[:,0])/1e3:.2f}, items {np.median(d[:,1])/1e3:.2f}, "
-              f"grid.sync {np.median(d[:,2])/1e3:.2f}, post {np.median(d[:,3])/1e3:.2f} us (block 0)")
+        md = lambda x: np.median(x) / 1e3  # noqa: E731
+        print(f"N={n} M={m} K={k} {arith.value}: per iteration {md(total):.2f} us; "
+              f"prologue {md(o[:,1]-o[:,0]):.2f}, items {md(o[:,2]-o[:,1]):.2f} "
+              f"[first item: begin {md(o[:,5]-o[:,1]):.2f}, leaves {md(o[:,6]-o[:,5]):.2f}, "
+              f"barrier {md(o[:,7]-o[:,6]):.2f}, finish {md(o[:,8]-o[:,7]):.2f}], "
+              f"grid.sync {md(o[:,3]-o[:,2]):.2f}, post {md(o[:,4]-o[:,3]):.2f} us (block 0)")
