@@ -76,6 +76,10 @@ _PROTOS = [
     ("dse_solve_resume", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
     ("dse_sweeper_stats", ctypes.c_int, [ctypes.c_void_p, i64p, i64p, i64p, i32p, i64p]),
     ("dse_fp64_peak", ctypes.c_int, [ctypes.c_int, f64p, ctypes.POINTER(DseErr)]),
+    ("dse_solve_batch", ctypes.c_int, [ctypes.POINTER(DseGrid), ctypes.POINTER(DseParams), ctypes.c_int64,
+                                       ctypes.c_int, ctypes.c_int, ctypes.c_int, f64p, ctypes.c_int64, f64p, f64p,
+                                       i64p, ctypes.POINTER(ctypes.c_int), f64p, ctypes.c_int64,
+                                       ctypes.POINTER(DseErr)]),
     ("dse_row_rhs", ctypes.c_int, [ctypes.POINTER(DseGrid), ctypes.POINTER(DseParams), ctypes.c_int, ctypes.c_int,
                                    ctypes.c_double, ctypes.c_double, ctypes.c_double, f64p, f64p, ctypes.c_int64,
                                    f64p, f64p, ctypes.POINTER(DseErr)]),

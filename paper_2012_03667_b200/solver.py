@@ -44,6 +44,7 @@ __all__ = [
     "resolve_threads",
     "iterate_once",
     "solve",
+    "solve_batch",
     "GpuSweeper",
     "DEFAULT_PROBES_LOG10P",
 ]
@@ -350,6 +351,66 @@ def solve(params: ModelParams, variant: AlgorithmVariant, grid: MomentumGrid | N
                                tuple(float(x) for x in r[3 + P:3 + 2 * P])) for r in hist]
     return PropagatorSolution(A=a, B=b, iterations=n, converged=conv, history=history, grid=grid,
                               params=params, probes_log10p=tuple(probes_log10p))
+
+
+def solve_batch(params_list, variant: AlgorithmVariant, grid: MomentumGrid | None = None,
+                probes_log10p: tuple[float, ...] = DEFAULT_PROBES_LOG10P, a0s=None, b0s=None) -> list:
+    """Independent solves on one grid in one go (parameter scans).
+
+    Equivalent to [solve(p, variant, grid, probes_log10p, a0, b0) for ...]
+    (bitwise: each solve runs the same kernel, concurrently on its own
+    stream with a share of the GPU).  The grid-defining fields (N, m_rad,
+    m_ang, p2_min, p2_max) must agree when grid is None.
+    """
+    params_list = list(params_list)
+    if not params_list:
+        return []
+    for prm in params_list:
+        prm.validate()
+    if resolve_threads(variant) != 1:
+        raise ParameterError("solve_batch runs on one GPU; use torchrun + solve for multi-GPU solves")
+    p0 = params_list[0]
+    if grid is None:
+        keys = {(p.N, p.m_rad, p.m_ang, p.p2_min, p.p2_max) for p in params_list}
+        if len(keys) != 1:
+            raise ParameterError("solve_batch needs one grid: N, m_rad, m_ang, p2_min, p2_max must agree")
+        grid = build_grid(p0.N, p0.m_rad, p0.m_ang, p0.p2_min, p0.p2_max)
+    S, n = len(params_list), grid.n_ext
+    A = np.ones((S, n)) if a0s is None else np.array(a0s, dtype=np.float64).reshape(S, n).copy()
+    B = np.ones((S, n)) if b0s is None else np.array(b0s, dtype=np.float64).reshape(S, n).copy()
+    probes_p2 = np.array([10.0 ** (2.0 * lp) for lp in probes_log10p], dtype=np.float64)
+    P = probes_p2.size
+    W = 3 + 2 * P
+    cap_max = max(int(p.max_iterations) for p in params_list)
+    hist = np.full((S, cap_max + 1, W), np.nan)
+    keep = [nat.as_f64(grid.p2_ext), nat.as_f64(grid.q2_int), nat.as_f64(grid.sqrt_q2_int),
+            nat.as_f64(grid.radial_measure), nat.as_i64(grid.bracket_idx), nat.as_f64(grid.z_nodes),
+            nat.as_f64(grid.z_weights)]
+    g = nat.DseGrid(*(p for _, p in keep), grid.n_ext, grid.m_rad, grid.m_ang)
+    prms = (nat.DseParams * S)(*[_c_params(p) for p in params_list])
+    its = np.zeros(S, np.int64)
+    conv = (ctypes.c_int * S)()
+    errs = (nat.DseErr * S)()
+    strat = nat.INTERP_INDEXED if variant.interp is InterpStrategy.PRECOMPUTED_INDEX else nat.INTERP_SEARCH
+    ar = nat.ARITH_FAST if variant.arith is Arithmetic.FAST else nat.ARITH_EXACT
+    rc = nat.load().dse_solve_batch(ctypes.byref(g), prms, S, strat, ar, _device(), probes_p2.ctypes.data_as(nat.f64p),
+                                    P, A.ctypes.data_as(nat.f64p), B.ctypes.data_as(nat.f64p),
+                                    its.ctypes.data_as(nat.i64p), conv, hist.ctypes.data_as(nat.f64p),
+                                    (cap_max + 1) * W, errs)
+    if rc:
+        for k in range(S):
+            if errs[k].code:
+                nat.raise_for(errs[k].code, errs[k])
+        nat.raise_for(rc, errs[0])
+    out = []
+    for k, prm in enumerate(params_list):
+        nk = int(its[k])
+        h = hist[k, : nk + 1]
+        records = [IterationRecord(int(r[0]), float(r[1]), float(r[2]), tuple(float(x) for x in r[3:3 + P]),
+                                   tuple(float(x) for x in r[3 + P:3 + 2 * P])) for r in h]
+        out.append(PropagatorSolution(A=A[k].copy(), B=B[k].copy(), iterations=nk, converged=bool(conv[k]),
+                                      history=records, grid=grid, params=prm, probes_log10p=tuple(probes_log10p)))
+    return out
 
 
 def _row_rhs_gpu(p2, a_p, b_p, a_q, b_q, grid, params, row, arith: Arithmetic = Arithmetic.EXACT):

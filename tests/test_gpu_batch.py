@@ -1,0 +1,46 @@
+"""GPU: batched independent solves (solve_batch) equal the individual solves
+bitwise -- iterations, converged flags, A, B and the full history."""
+import numpy as np
+import pytest
+
+import paper_2012_03667_b200 as p
+from conftest import golden, golden_grid, params_ns
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(x, y):
+    assert x.iterations == y.iterations and x.converged == y.converged
+    assert np.array_equal(x.A, y.A) and np.array_equal(x.B, y.B)
+    hx = np.array([[r.iteration, r.max_delta_a, r.max_delta_b, *r.probe_a, *r.probe_b] for r in x.history])
+    hy = np.array([[r.iteration, r.max_delta_a, r.max_delta_b, *r.probe_a, *r.probe_b] for r in y.history])
+    assert np.array_equal(hx, hy, equal_nan=True)
+
+
+@pytest.mark.parametrize("vname", ["indexed-gpu", "search-gpu-exact"])
+def test_batch_equals_individual_solves(vname):
+    g = golden_grid("default")
+    plist = [params_ns(D=d, m0=m0, relaxation=r, xi=1e-6, max_iterations=cap)
+             for d, m0, r, cap in ((0.55, 0.0, 1.0, 200), (0.45, 0.005, 1.0, 200), (0.65, 0.0, 0.7, 300),
+                                   (0.0, 0.01, 1.0, 50), (0.55, 0.0, 1.0, 3), (0.6, 0.002, 0.9, 250))]
+    b0s = np.stack([np.full(g.n_ext, b) for b in (0.3, 1.0, 0.5, 1.0, 0.3, 0.8)])
+    batch = p.solve_batch(plist, p.VARIANTS[vname], grid=g, b0s=b0s)
+    for prm, b0, got in zip(plist, b0s, batch):
+        _same(got, p.solve(prm, p.VARIANTS[vname], grid=g, b0=b0))
+    assert batch[3].iterations <= 2 and np.all(batch[3].A == 1.0)   # free theory
+    assert batch[4].iterations == 3 and not batch[4].converged       # cap
+
+
+def test_batch_config0_scan():
+    z = golden("solve_c0.npz")
+    g = golden_grid("c0")
+    plist = [params_ns(D=d, xi=1e-10, max_iterations=20000) for d in (0.55, 0.5, 0.6)]
+    sols = p.solve_batch(plist, p.VARIANTS["indexed-gpu"], grid=g, b0s=np.full((3, g.n_ext), 0.3))
+    assert sols[0].iterations == int(z["iterations"]) == 2923 and sols[0].converged
+    assert all(s.converged for s in sols)
+
+
+def test_batch_validation():
+    with pytest.raises(p.ParameterError):
+        p.solve_batch([p.ModelParams(N=20), p.ModelParams(N=30)], p.VARIANTS["indexed-gpu"])
+    assert p.solve_batch([], p.VARIANTS["indexed-gpu"]) == []
