@@ -222,6 +222,8 @@ def run_ours(args):
         extra["time_to_solution"] = time_to_solution(p, torch, dev, arith)
     if not args.no_interp:
         extra["interp_config1"] = interp_bench(p, nat, torch, dev, peak_hbm())
+    if not args.no_tts:
+        extra["batched_scan"] = batch_bench(p)
     cpu = None
     if not args.no_cpu:
         rate, info = cpu_port_rate(grid, params, float(os.environ.get("BENCH_CPU_S", "10")),
@@ -336,6 +338,29 @@ def time_to_solution(p, torch, dev, arith):
                      "seconds_wall": wall, "points_per_s": pts / wall}
         sw.close()
     return out
+
+
+def batch_bench(p):
+    """Parameter scan on the config-0 grid: 16 independent solves (D in
+    [0.50, 0.60], b0 = 0.3, xi = 1e-10, cap 20000) through solve_batch, vs the
+    same 16 solves one after another."""
+    g = p.build_grid(128, 128, 64, 1e-6, 1e4)
+    ds = np.linspace(0.50, 0.60, 16)
+    plist = [p.ModelParams(N=128, m_rad=128, m_ang=64, D=float(d), xi=1e-10, max_iterations=20000) for d in ds]
+    b0s = np.full((len(ds), 128), 0.3)
+    v = p.VARIANTS["indexed-gpu"]
+    p.solve_batch(plist[:2], v, grid=g, b0s=b0s[:2])
+    t0 = time.perf_counter()
+    sols = p.solve_batch(plist, v, grid=g, b0s=b0s)
+    tb = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for prm in plist:
+        p.solve(prm, v, grid=g, b0=np.full(128, 0.3))
+    ts = time.perf_counter() - t0
+    its = [s.iterations for s in sols]
+    return {"solves": len(ds), "seconds_batched": tb, "seconds_sequential": ts, "solves_per_s": len(ds) / tb,
+            "iterations": its, "converged": int(sum(s.converged for s in sols)),
+            "points_per_s": float(sum(its)) * 128 * 128 * 64 / tb}
 
 
 def interp_bench(p, nat, torch, dev, hbm):

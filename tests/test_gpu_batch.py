@@ -34,10 +34,11 @@ def test_batch_equals_individual_solves(vname):
 def test_batch_config0_scan():
     z = golden("solve_c0.npz")
     g = golden_grid("c0")
-    plist = [params_ns(D=d, xi=1e-10, max_iterations=20000) for d in (0.55, 0.5, 0.6)]
+    plist = [params_ns(D=d, xi=1e-10, max_iterations=4000) for d in (0.55, 0.5, 0.6)]
     sols = p.solve_batch(plist, p.VARIANTS["indexed-gpu"], grid=g, b0s=np.full((3, g.n_ext), 0.3))
     assert sols[0].iterations == int(z["iterations"]) == 2923 and sols[0].converged
-    assert all(s.converged for s in sols)
+    for prm, got in zip(plist[1:], sols[1:]):
+        _same(got, p.solve(prm, p.VARIANTS["indexed-gpu"], grid=g, b0=np.full(g.n_ext, 0.3)))
 
 
 def test_batch_validation():
