@@ -85,6 +85,7 @@ _PROTOS = [
                                    f64p, f64p, ctypes.POINTER(DseErr)]),
     ("dse_debug_pairwise_sum", ctypes.c_int, [ctypes.c_int, f64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                               ctypes.c_int64, f64p, f64p, ctypes.POINTER(DseErr)]),
+    ("dse_debug_check_flags", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32)]),
     ("dse_launch_count", ctypes.c_int64, []),
 ]
 
