@@ -17,8 +17,19 @@ def _same(x, y):
     assert np.array_equal(hx, hy, equal_nan=True)
 
 
+@pytest.fixture(params=["kernel", "streams"])
+def batch_mode(request, monkeypatch):
+    """dse_solve_batch has two implementations: one batched cooperative kernel
+    (default) and concurrent per-solve kernels on streams (fallback)."""
+    if request.param == "streams":
+        monkeypatch.setenv("DSE_BATCH_STREAMS", "1")
+    else:
+        monkeypatch.delenv("DSE_BATCH_STREAMS", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("vname", ["indexed-gpu", "search-gpu-exact"])
-def test_batch_equals_individual_solves(vname):
+def test_batch_equals_individual_solves(vname, batch_mode):
     g = golden_grid("default")
     plist = [params_ns(D=d, m0=m0, relaxation=r, xi=1e-6, max_iterations=cap)
              for d, m0, r, cap in ((0.55, 0.0, 1.0, 200), (0.45, 0.005, 1.0, 200), (0.65, 0.0, 0.7, 300),
@@ -31,7 +42,7 @@ def test_batch_equals_individual_solves(vname):
     assert batch[4].iterations == 3 and not batch[4].converged       # cap
 
 
-def test_batch_config0_scan():
+def test_batch_config0_scan(batch_mode):
     z = golden("solve_c0.npz")
     g = golden_grid("c0")
     plist = [params_ns(D=d, xi=1e-10, max_iterations=4000) for d in (0.55, 0.5, 0.6)]
@@ -45,3 +56,19 @@ def test_batch_validation():
     with pytest.raises(p.ParameterError):
         p.solve_batch([p.ModelParams(N=20), p.ModelParams(N=30)], p.VARIANTS["indexed-gpu"])
     assert p.solve_batch([], p.VARIANTS["indexed-gpu"]) == []
+
+
+def test_batch_failure_is_per_solve_and_located(batch_mode):
+    g = golden_grid("small")
+    b0s = np.full((2, g.n_ext), 0.3)
+    a0s = np.ones((2, g.n_ext))
+    a0s[1, 5] = np.inf
+    with pytest.raises(p.NumericalFailureError) as ei:
+        p.solve_batch([params_ns(xi=1e-3, max_iterations=5)] * 2, p.VARIANTS["indexed-gpu"], grid=g, a0s=a0s, b0s=b0s)
+    single = None
+    try:
+        p.solve(params_ns(xi=1e-3, max_iterations=5), p.VARIANTS["indexed-gpu"], grid=g, a0=a0s[1], b0=b0s[1])
+    except p.NumericalFailureError as exc:
+        single = exc
+    assert single is not None
+    assert (ei.value.row, ei.value.radial, ei.value.angular) == (single.row, single.radial, single.angular)
