@@ -341,15 +341,18 @@ def time_to_solution(p, torch, dev, arith):
 
 
 def batch_bench(p):
-    """Parameter scan on the config-0 grid: 16 independent solves (D in
-    [0.50, 0.60], b0 = 0.3, xi = 1e-10, cap 20000) through solve_batch, vs the
-    same 16 solves one after another."""
+    """Parameter scan on the config-0 grid (the vacuum analogue of BASELINE
+    config 4's batched solves): 32 independent solves, D uniform in [0.40,
+    0.50], b0 = 0.3, xi = 1e-10, cap 20000, through solve_batch (one batched
+    cooperative kernel), vs the same 32 solves one after another."""
     g = p.build_grid(128, 128, 64, 1e-6, 1e4)
-    ds = np.linspace(0.50, 0.60, 16)
+    ds = np.linspace(0.40, 0.50, 32)
     plist = [p.ModelParams(N=128, m_rad=128, m_ang=64, D=float(d), xi=1e-10, max_iterations=20000) for d in ds]
     b0s = np.full((len(ds), 128), 0.3)
     v = p.VARIANTS["indexed-gpu"]
     p.solve_batch(plist[:2], v, grid=g, b0s=b0s[:2])
+    for prm in plist[:2]:
+        p.solve(prm, v, grid=g, b0=np.full(128, 0.3))
     t0 = time.perf_counter()
     sols = p.solve_batch(plist, v, grid=g, b0s=b0s)
     tb = time.perf_counter() - t0
