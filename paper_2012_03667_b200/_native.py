@@ -85,6 +85,8 @@ _PROTOS = [
                                    f64p, f64p, ctypes.POINTER(DseErr)]),
     ("dse_debug_pairwise_sum", ctypes.c_int, [ctypes.c_int, f64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                               ctypes.c_int64, f64p, f64p, ctypes.POINTER(DseErr)]),
+    ("dse_plan_info", ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, i32p, i32p, ctypes.c_int64, i32p, i32p, i32p,
+                                     ctypes.c_int64, i64p, i64p]),
     ("dse_debug_check_flags", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32)]),
     ("dse_launch_count", ctypes.c_int64, []),
 ]
@@ -162,3 +164,18 @@ def debug_pairwise_sum(vals, chunk_leaves: int = 0, device: int = 0):
                                        oa.ctypes.data_as(f64p), ob.ctypes.data_as(f64p), _ct.byref(err))
     raise_for(rc, err)
     return oa, ob
+
+
+def plan_info(n: int, chunk_leaves: int = 1 << 30):
+    """The kernels' reduction plan for an n-element block (host only)."""
+    import ctypes as _ct
+    cap = n // 64 + 8
+    ls, ll = np.zeros(cap, np.int32), np.zeros(cap, np.int32)
+    lo, hi, tp = np.zeros(cap, np.int32), np.zeros(cap, np.int32), np.zeros(2 * cap, np.int32)
+    nl, nc = _ct.c_int64(), _ct.c_int64()
+    rc = load().dse_plan_info(n, chunk_leaves, ls.ctypes.data_as(i32p), ll.ctypes.data_as(i32p), cap,
+                              lo.ctypes.data_as(i32p), hi.ctypes.data_as(i32p), tp.ctypes.data_as(i32p), cap,
+                              _ct.byref(nl), _ct.byref(nc))
+    if rc:
+        raise ValueError(f"dse_plan_info failed ({rc})")
+    return (ls[:nl.value], ll[:nl.value], lo[:nc.value], hi[:nc.value], tp[:2 * max(nc.value - 1, 0)].reshape(-1, 2))
