@@ -78,24 +78,33 @@ class ShardedLoop:
     def sweep(self, a, b):
         return self._assemble(*self.sweep_rows(a, b))
 
-    def run(self, a, b, xi: float, cap: int, relaxation: float):
+    def run(self, a, b, xi: float, cap: int, relaxation: float, check_every: int = 16):
+        """successive_approximation with a lazy stop test: the deltas, probes
+        and states of the last `check_every` iterations stay on the device and
+        the host looks at them once per window (one sync per window instead of
+        one per iteration).  The result is that of the eager loop: the solve
+        stops at the FIRST iteration whose deltas are both < xi, and that
+        iteration's state is returned."""
         xp = self.xp
         hist = [[0.0, math.nan, math.nan, *self._probe_row(a, b)]]
-        converged = False
-        n_done = cap
+        window = []  # (iteration, a, b, da, db, probes) kept as device values
         for it in range(1, cap + 1):
             an, bn = self.sweep(a, b)
             if relaxation != 1.0:
                 an = relaxation * an + (1.0 - relaxation) * a
                 bn = relaxation * bn + (1.0 - relaxation) * b
-            da = float(xp.max(xp.abs(an - a)))
-            db = float(xp.max(xp.abs(bn - b)))
+            da = xp.max(xp.abs(an - a))
+            db = xp.max(xp.abs(bn - b))
             a, b = an, bn
-            hist.append([float(it), da, db, *self._probe_row(a, b)])
-            if da < xi and db < xi:
-                converged, n_done = True, it
-                break
-        return a, b, n_done, converged, np.array(hist)
+            window.append((it, a, b, da, db, self.probe(a, b)))
+            if len(window) == check_every or it == cap:
+                for (n, wa, wb, wda, wdb, (pa, pb)) in window:   # host reads the window once
+                    fda, fdb = float(wda), float(wdb)
+                    hist.append([float(n), fda, fdb, *[float(x) for x in pa], *[float(x) for x in pb]])
+                    if fda < xi and fdb < xi:
+                        return wa, wb, n, True, np.array(hist)
+                window = []
+        return a, b, cap, False, np.array(hist)
 
     def _probe_row(self, a, b):
         pa, pb = self.probe(a, b)
@@ -139,8 +148,6 @@ def _device_loop(grid, params, variant):
         dist.all_gather_into_tensor(out, buf.contiguous())
         return out
 
-    probes_dev = {}
-
     def probe_fn(probes_p2):
         pr = torch.tensor(list(probes_p2), dtype=torch.float64, device=dev)
 
@@ -155,7 +162,7 @@ def _device_loop(grid, params, variant):
                     p2.data_ptr(), v.data_ptr(), grid.n_ext, pr.data_ptr(), len(probes_p2), nat.BATCH_SEARCH,
                     o.data_ptr(), None, torch.cuda.current_stream(dev).cuda_stream, ctypes.byref(err))
                 nat.raise_for(rc, err)
-                res.append(o.cpu().numpy())
+                res.append(o)  # stays on the device; read at the stop-test window
             return res[0], res[1]
         return probe
 

@@ -44,7 +44,7 @@ def _run(rank, world, port, q):
         return np.stack([t.numpy() for t in parts])
 
     loop = ShardedLoop(N, rank, world, sweep_rows, gather, probe)
-    res = loop.run(np.ones(N), np.full(N, 0.3), 1e-12, 200, 0.5)
+    res = loop.run(np.ones(N), np.full(N, 0.3), 1e-12, 200, 0.5, check_every=7)
     q.put((rank, res))
     dist.destroy_process_group()
 
@@ -55,9 +55,18 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _single():
+def _single(check_every=1):
     loop = ShardedLoop(N, 0, 1, lambda a, b: jacobi_map(a, b), lambda buf: buf[None], probe)
-    return loop.run(np.ones(N), np.full(N, 0.3), 1e-12, 200, 0.5)
+    return loop.run(np.ones(N), np.full(N, 0.3), 1e-12, 200, 0.5, check_every=check_every)
+
+
+@pytest.mark.parametrize("window", [1, 3, 16, 1000])
+def test_lazy_stop_test_equals_eager(window):
+    """The windowed stop test returns the eager loop's iteration, state and history."""
+    a1, b1, n1, c1, h1 = _single(1)
+    a2, b2, n2, c2, h2 = _single(window)
+    assert (n1, c1) == (n2, c2) and np.array_equal(a1, a2) and np.array_equal(b1, b2)
+    assert np.array_equal(h1, h2, equal_nan=True)
 
 
 @pytest.mark.parametrize("world", [2, 3])
