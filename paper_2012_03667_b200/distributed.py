@@ -194,15 +194,20 @@ def iterate_once_sharded(grid, a, b, params, variant):
 
 
 def bench_main(args, metric, unit, cfg, flop_per_point):
-    """bench.py under torchrun: weak-scaling-free strong split of config 2 rows
-    across ranks; each step = local sweep + NCCL all-gather + convergence test.
-    Timed with CUDA events on every rank, max over ranks."""
+    """bench.py under torchrun: config 2's rows split cyclically over the
+    ranks (a fixed problem: strong scaling); each step = local sweep of the
+    owned rows + NCCL all-gather + relaxation/max-norm deltas on every rank,
+    from the same synthetic state.  L2 flushed before every timed step, CUDA
+    events on every rank, max over ranks.  e2e: the public iterate_once with
+    pinned host buffers through the same sharded path."""
     import json
+    import time
 
     import torch
     import torch.distributed as dist
 
-    from . import build_grid, ModelParams, VARIANTS
+    from . import VARIANTS, ModelParams, build_grid, iterate_once
+    from . import _native as nat
     dist.init_process_group("nccl")
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -215,25 +220,60 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
     loop = ShardedLoop(grid.n_ext, rank, world, sweep_rows, gather, probe_fn(()), xp=torch)
     a = torch.ones(grid.n_ext, dtype=torch.float64, device=dev)
     b = torch.full((grid.n_ext,), 0.3, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step():
+        an, bn = loop.sweep(a, b)
+        return torch.max(torch.abs(an - a)), torch.max(torch.abs(bn - b))
+
     for _ in range(args.warmup):
-        an, bn = loop.sweep(a, b)
+        flush.fill_(1)
+        step()
     torch.cuda.synchronize()
     dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        an, bn = loop.sweep(a, b)
-        da = torch.max(torch.abs(an - a))
-        db = torch.max(torch.abs(bn - b))
-        a, b = an, bn
-    e1.record()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = nat.launch_count()
+    clk = None
+    if rank == 0:
+        from bench import ClockSampler  # the repo's bench.py (rank 0 samples its GPU's clocks)
+        clk = ClockSampler(local).__enter__()
+    for e0, e1 in ev:
+        flush.fill_(1)
+        e0.record()
+        step()
+        e1.record()
     torch.cuda.synchronize()
+    if clk is not None:
+        clk.__exit__(None, None, None)
+    launches = nat.launch_count() - launches0
     dist.barrier()
-    t = torch.tensor([e0.elapsed_time(e1) / 1e3], device=dev)
+    t = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in ev) / 1e3], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t = float(t.item())
     st = sw.stats()
+    evald = torch.tensor([float(st["evaluated_points"])], device=dev)
+    dist.all_reduce(evald, op=dist.ReduceOp.SUM)
     nominal = cfg["N"] * cfg["M"] * cfg["K"]
+    # e2e through the public API (pinned host arrays, H2D + D2H every step)
+    a_h = torch.ones(grid.n_ext, dtype=torch.float64).pin_memory().numpy()
+    b_h = torch.full((grid.n_ext,), 0.3, dtype=torch.float64).pin_memory().numpy()
+    iterate_once(grid, a_h, b_h, params, variant)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        iterate_once(grid, a_h, b_h, params, variant)
+    te = torch.tensor([time.perf_counter() - t0], device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    peak = None
+    try:
+        import ctypes
+        v = ctypes.c_double(0)
+        err = nat.DseErr()
+        if nat.load().dse_fp64_peak(local, ctypes.byref(v), ctypes.byref(err)) == 0:
+            peak = v.value
+    except Exception:  # noqa: BLE001
+        peak = None
+    achieved = float(evald.item()) * flop_per_point / t * args.steps / 1e12 / world  # per GPU
     if rank == 0:
         print(json.dumps({
             "metric": metric, "value": nominal * args.steps / t, "unit": unit, "n_gpus": world,
@@ -242,7 +282,18 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
             "data": "synthetic",
             "config": {"workload": "config2_vacuum_1024x1024x256", "parallelism": f"rows cyclic over {world} GPUs",
                        "collective": "NCCL all_gather of [A'|B'] rows per step",
-                       "evaluated_points_rank0": st["evaluated_points"]},
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "evaluated_points_per_step": int(evald.item()), "nominal_points_per_step": nominal},
+            "e2e": {"value": nominal * args.steps / float(te.item()), "unit": unit,
+                    "h2d_bytes_per_step": 2 * grid.n_ext * 8, "d2h_bytes_per_step": 2 * grid.n_ext * 8,
+                    "api": "paper_2012_03667_b200.iterate_once(grid, A, B, params, "
+                           "VARIANTS['indexed-gpu'].with_threads(W)) under torchrun"},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "flop_per_point": flop_per_point, "points": "evaluated, per GPU",
+                         "peak_source": "measured: dse_fp64_peak DFMA probe (per GPU)"},
+            "gpu_launches": launches,
+            "clocks": clk.summary() if clk is not None else None,
         }))
     sw.close()
     dist.destroy_process_group()
