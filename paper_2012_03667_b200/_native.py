@@ -43,6 +43,11 @@ class DseErr(ctypes.Structure):
                 ("radial", ctypes.c_int64), ("angular", ctypes.c_int64), ("msg", ctypes.c_char * 256)]
 
 
+class DseLayout(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("threads", "lanes_per_leaf", "static_items", "cluster2",
+                                              "split_rows", "node_chunk")]
+
+
 _LIB = None
 
 # (name, restype, argtypes) -- one row per declaration in include/dse_b200.h
@@ -75,6 +80,7 @@ _PROTOS = [
                                       ctypes.POINTER(DseErr)]),
     ("dse_solve_resume", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
     ("dse_sweeper_stats", ctypes.c_int, [ctypes.c_void_p, i64p, i64p, i64p, i32p, i64p]),
+    ("dse_sweeper_layout", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     ("dse_fp64_peak", ctypes.c_int, [ctypes.c_int, f64p, ctypes.POINTER(DseErr)]),
     ("dse_solve_batch", ctypes.c_int, [ctypes.POINTER(DseGrid), ctypes.POINTER(DseParams), ctypes.c_int64,
                                        ctypes.c_int, ctypes.c_int, ctypes.c_int, f64p, ctypes.c_int64, f64p, f64p,

@@ -265,6 +265,12 @@ class GpuSweeper:
         return {"nominal_points": nom.value, "evaluated_points": ev.value, "rows": rows.value,
                 "blocks": blocks.value, "smem_bytes": smem.value}
 
+    def layout(self) -> dict:
+        """The execution layout the library chose (dse_sweeper_layout)."""
+        out = nat.DseLayout()
+        self.lib.dse_sweeper_layout(self.handle, ctypes.byref(out))
+        return {n: getattr(out, n) for n, _ in out._fields_}
+
     def close(self):
         if getattr(self, "handle", None):
             self.lib.dse_sweeper_destroy(self.handle)

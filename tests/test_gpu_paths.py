@@ -1,0 +1,63 @@
+"""GPU: the fast sweep's execution layouts give bit-identical results.
+
+The many-rows regime can run 8 threads per leaf (one numpy lane sum each) or
+4 threads per leaf (two lane sums each), and rows may be split into subtree
+chunks.  All of these evaluate every lane sum with the same operation
+sequence and combine in numpy's tree order, so the outputs must agree bit for
+bit (the layout is chosen from the environment at launch: DSE_GL8,
+DSE_SPLIT_ROWS/DSE_CHUNK_LEAVES).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2012_03667_b200 as p
+
+pytestmark = pytest.mark.gpu
+
+# (N, M, K): power-of-two trees (32 leaves of 128, 64 of 72 elements), an
+# unequal-leaf tree (3000 elements: leaves of 88-96) and an irregularly shaped
+# one (132 x 32: subtrees of 264 split 128 | 64 + 72)
+GRIDS = [(400, 64, 64), (320, 96, 48), (350, 100, 30), (330, 132, 32)]
+
+
+def _sweep(g, prm, env, arith=p.Arithmetic.FAST):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, arith, 0)
+        try:
+            rng = np.random.default_rng(7)
+            a = 1.0 + 0.3 * rng.random(g.n_ext)
+            b = 0.2 + 0.2 * rng.random(g.n_ext)
+            ao, bo = sw.sweep(a, b)
+            return ao, bo, sw.layout()
+        finally:
+            sw.close()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("n,m,k", GRIDS)
+def test_layouts_bitwise_equal(n, m, k):
+    g = p.build_grid(n, m, k, 1e-4, 1e4)
+    prm = p.ModelParams(N=n, m_rad=m, m_ang=k, xi=1e-10)
+    a0, b0, lay = _sweep(g, prm, {})
+    assert lay["lanes_per_leaf"] == 4 and lay["static_items"] == 0 and lay["node_chunk"] > 0
+    variants = [{"DSE_GL8": "1"},
+                {"DSE_SPLIT_ROWS": "-1", "DSE_CHUNK_LEAVES": "8"},
+                {"DSE_SPLIT_ROWS": "-1", "DSE_CHUNK_LEAVES": "16", "DSE_GL8": "1"}]
+    for env in variants:
+        a1, b1, lay1 = _sweep(g, prm, env)
+        assert np.array_equal(a0, a1) and np.array_equal(b0, b1), (env, lay1)
+    assert _sweep(g, prm, variants[0])[2]["lanes_per_leaf"] == 8
+    assert _sweep(g, prm, variants[1])[2]["split_rows"] == n
+    # and the layouts agree with exact arithmetic to the fast-mode tolerance
+    ae, be, _ = _sweep(g, prm, {}, p.Arithmetic.EXACT)
+    assert np.max(np.abs(a0 - ae) / np.abs(ae)) < 1e-12
+    assert np.max(np.abs(b0 - be)) / np.max(np.abs(be)) < 1e-12
