@@ -222,6 +222,7 @@ def run_ours(args):
     extra = {}
     if not args.no_tts:
         extra["time_to_solution"] = time_to_solution(p, torch, dev, arith)
+        extra["moments"] = moments_bench(p, torch, dev, grid, params, stream, flush, args)
     if not args.no_interp:
         extra["interp_config1"] = interp_bench(p, nat, torch, dev, peak_hbm())
     if not args.no_tts:
@@ -340,6 +341,56 @@ def time_to_solution(p, torch, dev, arith):
         out[name] = {"iterations": it, "converged": conv, "seconds_device": e0.elapsed_time(e1) / 1e3,
                      "seconds_wall": wall, "points_per_s": pts / wall}
         sw.close()
+    return out
+
+
+def moments_bench(p, torch, dev, grid, params, stream, flush, args):
+    """The angular-moment factorisation (VARIANTS
+    'indexed-gpu-moments'): not the integrand-points metric (an iteration is
+    O(N M), not O(N M K)), so reported separately -- time to solution with
+    the one-off moment build (sweeper setup, wall clock) and the on-device
+    loop timed apart, and the per-iteration time at config 2."""
+    out = {}
+    cases = {
+        "config0_128x128x64": dict(N=128, m_rad=128, m_ang=64, xi=1e-10, max_iterations=20000),
+        "substitute_256x256x256_relax0.5": dict(N=256, m_rad=256, m_ang=256, xi=1e-10, max_iterations=2000,
+                                                relaxation=0.5),
+    }
+    for name, kw in cases.items():
+        prm = p.ModelParams(**kw)
+        g = p.build_grid(prm.N, prm.m_rad, prm.m_ang, prm.p2_min, prm.p2_max)
+        p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, p.Arithmetic.MOMENTS).close()  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, p.Arithmetic.MOMENTS)
+        setup = time.perf_counter() - t0
+        A = torch.ones(prm.N, dtype=torch.float64, device=dev)
+        B = torch.full((prm.N,), 0.3, dtype=torch.float64, device=dev)
+        sw.solve_device(A.data_ptr(), B.data_ptr(), prm.max_iterations)  # warm-up
+        A.fill_(1.0)
+        B.fill_(0.3)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        it, conv = sw.solve_device(A.data_ptr(), B.data_ptr(), prm.max_iterations)
+        e1.record()
+        torch.cuda.synchronize()
+        loop = e0.elapsed_time(e1) / 1e3
+        out[name] = {"iterations": it, "converged": conv, "seconds_device_loop": loop,
+                     "seconds_setup_wall": setup, "seconds_total": loop + setup}
+        sw.close()
+    p.GpuSweeper(grid, params, p.InterpStrategy.PRECOMPUTED_INDEX, p.Arithmetic.MOMENTS).close()  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sw = p.GpuSweeper(grid, params, p.InterpStrategy.PRECOMPUTED_INDEX, p.Arithmetic.MOMENTS)
+    setup = time.perf_counter() - t0
+    n = grid.n_ext
+    A0 = torch.ones(n, dtype=torch.float64, device=dev)
+    B0 = torch.full((n,), 0.3, dtype=torch.float64, device=dev)
+    ms = time_device_steps(torch, sw, A0, B0, stream, flush, min(args.steps, 50), args.warmup)
+    out["config2_1024x1024x256"] = {"ms_per_iteration": sum(ms) / len(ms), "seconds_setup_wall": setup,
+                                    "l2": "flushed before every timed step", "steps": len(ms)}
+    sw.close()
     return out
 
 

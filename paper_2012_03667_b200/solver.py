@@ -67,10 +67,21 @@ class Arithmetic(enum.Enum):
            device exp (<= 1 ulp).
     FAST:  algebraically reduced, FMA-contracted, one reciprocal of k2 per
            point (csrc/dse_device.cuh point_fast).
+    MOMENTS: the angular-moment factorisation: six
+           theta-moments per (row, radial node) built once per sweeper from
+           the grid and omega, then O(N*M) work per iteration
+           (dse_moment_kernel).  A different summation order: parity with the
+           reference to the fast tolerance, not bitwise.
     """
 
     EXACT = "exact"
     FAST = "fast"
+    MOMENTS = "moments"
+
+
+def _arith_code(arith: Arithmetic) -> int:
+    return {Arithmetic.EXACT: nat.ARITH_EXACT, Arithmetic.FAST: nat.ARITH_FAST,
+            Arithmetic.MOMENTS: nat.ARITH_MOMENTS}[arith]
 
 
 @dataclass(frozen=True)
@@ -105,6 +116,10 @@ VARIANTS = {
     # the reference's operation order, one rounding per numpy op
     "search-gpu-exact": _SEARCH.with_arith(Arithmetic.EXACT),
     "indexed-gpu-exact": _INDEXED.with_arith(Arithmetic.EXACT),
+    # the angular-moment factorisation: O(N M) per iteration after a one-off
+    # O(N M K) moment build (for solves; parity gated like the fast variants)
+    "search-gpu-moments": _SEARCH.with_arith(Arithmetic.MOMENTS),
+    "indexed-gpu-moments": _INDEXED.with_arith(Arithmetic.MOMENTS),
     # the reference's names (solver.py:69-74) -> the GPU variant with that
     # strategy, in the bit-faithful exact arithmetic
     "search-seq": _SEARCH.with_arith(Arithmetic.EXACT),
@@ -189,7 +204,7 @@ class GpuSweeper:
         handle = ctypes.c_void_p()
         err = nat.DseErr()
         strat = nat.INTERP_INDEXED if strategy is InterpStrategy.PRECOMPUTED_INDEX else nat.INTERP_SEARCH
-        ar = nat.ARITH_FAST if arith is Arithmetic.FAST else nat.ARITH_EXACT
+        ar = _arith_code(arith)
         rc = self.lib.dse_sweeper_create(ctypes.byref(g), ctypes.byref(prm), strat, ar, self.device,
                                          int(rows[0]), int(rows[1]), ctypes.byref(handle), ctypes.byref(err))
         nat.raise_for(rc, err)
@@ -398,7 +413,7 @@ def solve_batch(params_list, variant: AlgorithmVariant, grid: MomentumGrid | Non
     conv = (ctypes.c_int * S)()
     errs = (nat.DseErr * S)()
     strat = nat.INTERP_INDEXED if variant.interp is InterpStrategy.PRECOMPUTED_INDEX else nat.INTERP_SEARCH
-    ar = nat.ARITH_FAST if variant.arith is Arithmetic.FAST else nat.ARITH_EXACT
+    ar = _arith_code(variant.arith)
     rc = nat.load().dse_solve_batch(ctypes.byref(g), prms, S, strat, ar, _device(), probes_p2.ctypes.data_as(nat.f64p),
                                     P, A.ctypes.data_as(nat.f64p), B.ctypes.data_as(nat.f64p),
                                     its.ctypes.data_as(nat.i64p), conv, hist.ctypes.data_as(nat.f64p),
@@ -434,8 +449,7 @@ def _row_rhs_gpu(p2, a_p, b_p, a_q, b_q, grid, params, row, arith: Arithmetic = 
     prm = _c_params(params)
     oa, ob = ctypes.c_double(), ctypes.c_double()
     err = nat.DseErr()
-    rc = lib.dse_row_rhs(ctypes.byref(g), ctypes.byref(prm), nat.ARITH_FAST if arith is Arithmetic.FAST else
-                         nat.ARITH_EXACT, _device(), float(p2), float(a_p), float(b_p), paq, pbq,
+    rc = lib.dse_row_rhs(ctypes.byref(g), ctypes.byref(prm), _arith_code(arith), _device(), float(p2), float(a_p), float(b_p), paq, pbq,
                          -1 if row is None else int(row), ctypes.byref(oa), ctypes.byref(ob), ctypes.byref(err))
     if rc == nat.DSE_ENUMERIC and row is None:
         err.row = -1

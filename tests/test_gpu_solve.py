@@ -26,7 +26,7 @@ def _hist(sol):
     return np.array([[r.iteration, r.max_delta_a, r.max_delta_b, *r.probe_a, *r.probe_b] for r in sol.history])
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "search-gpu-exact", "indexed-gpu"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "search-gpu-exact", "indexed-gpu", "indexed-gpu-moments"])
 def test_solve_default_config(vname):
     z, sol = _run("solve_default.npz", "default", p.VARIANTS[vname])
     assert sol.iterations == int(z["iterations"]) and sol.converged == bool(z["converged"])
@@ -38,7 +38,8 @@ def test_solve_default_config(vname):
     np.testing.assert_allclose(h[:, 3:], z["history"][:, 3:], rtol=1e-11)
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu", "indexed-gpu-moments",
+                                   "search-gpu-moments"])
 def test_solve_config0_exact_iteration_count(vname):
     """Config 0 (128/128/64, xi=1e-10, b0=0.3): the reference converges in 2923 sweeps."""
     z, sol = _run("solve_c0.npz", "c0", p.VARIANTS[vname])
@@ -48,7 +49,7 @@ def test_solve_config0_exact_iteration_count(vname):
     assert h.shape == z["history"].shape
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu", "indexed-gpu-moments"])
 def test_solve_config2_first_10_sweeps(vname):
     """Config 2 (1024/1024/256) does not converge in the reference:
     parity = first 10 sweeps + converged=False at the same cap."""
@@ -58,7 +59,7 @@ def test_solve_config2_first_10_sweeps(vname):
     np.testing.assert_allclose(_hist(sol)[1:, 1:3], z["history"][1:, 1:3], rtol=1e-6)
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu", "indexed-gpu-moments"])
 def test_solve_large_substitute_relaxation(vname):
     """N=M=K=256 at relaxation 0.5: the reference converges in 421 iterations."""
     z, sol = _run("solve_sub256.npz", "sub256", p.VARIANTS[vname])
@@ -85,3 +86,45 @@ def test_solve_numerical_failure_raises():
     with pytest.raises(p.NumericalFailureError) as ei:
         p.solve(params_ns(xi=1e-3, max_iterations=5), p.VARIANTS["indexed-gpu-exact"], grid=g, a0=a0)
     assert ei.value.iteration == 1 and ei.value.row is not None
+
+
+def test_moments_batch_equals_standalone():
+    """Batched solves with the moments arithmetic (concurrent per-solve
+    sweepers) equal the standalone solves bitwise."""
+    g = golden_grid("c0")
+    v = p.VARIANTS["indexed-gpu-moments"]
+    prms = [p.ModelParams(N=128, m_rad=128, m_ang=64, xi=1e-10, max_iterations=5000, D=D) for D in (0.5, 0.6)]
+    batch = p.solve_batch(prms, v, grid=g, b0s=[np.full(g.n_ext, 0.3)] * 2)
+    for prm, sb in zip(prms, batch):
+        s1 = p.solve(prm, v, grid=g, b0=np.full(g.n_ext, 0.3))
+        assert sb.iterations == s1.iterations and sb.converged == s1.converged
+        assert np.array_equal(sb.A, s1.A) and np.array_equal(sb.B, s1.B)
+
+
+@pytest.mark.parametrize("arith", [p.Arithmetic.EXACT, p.Arithmetic.FAST, p.Arithmetic.MOMENTS])
+def test_load_resume_status_protocol(arith):
+    """dse_solve_load + dse_solve_resume on a fresh sweeper (no sweep/solve
+    first): a clean run checks clean, a non-finite state reports the reference
+    location, and a following clean load/resume is clean again."""
+    import torch
+
+    E = golden("errors.npz")
+    g = golden_grid("small")
+    name = str(E["names"][0])
+    for _ in range(3):  # fresh sweepers, possibly on recycled device memory
+        sw = p.GpuSweeper(g, params_ns(), p.InterpStrategy.PRECOMPUTED_INDEX, arith)
+        good = (torch.ones(g.n_ext, dtype=torch.float64, device="cuda"),
+                torch.full((g.n_ext,), 0.3, dtype=torch.float64, device="cuda"))
+        bad = (torch.as_tensor(E[f"{name}__a"], device="cuda"), torch.as_tensor(E[f"{name}__b"], device="cuda"))
+        sw.load_device(good[0].data_ptr(), good[1].data_ptr())
+        sw.resume(3)
+        sw.check()
+        sw.load_device(bad[0].data_ptr(), bad[1].data_ptr())
+        sw.resume(1)
+        with pytest.raises(p.NumericalFailureError) as ei:
+            sw.check()
+        assert (ei.value.row, ei.value.radial, ei.value.angular) == tuple(int(v) for v in E[f"{name}__loc"])
+        sw.load_device(good[0].data_ptr(), good[1].data_ptr())
+        sw.resume(2)
+        sw.check()
+        sw.close()

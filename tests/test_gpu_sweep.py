@@ -16,8 +16,9 @@ from conftest import golden, golden_grid, hybrid_rel, params_ns
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"exact": 1e-13, "fast": 1e-12}
-VAR = {"exact": p.VARIANTS["indexed-gpu-exact"], "fast": p.VARIANTS["indexed-gpu"]}
+TOL = {"exact": 1e-13, "fast": 1e-12, "moments": 1e-12}
+VAR = {"exact": p.VARIANTS["indexed-gpu-exact"], "fast": p.VARIANTS["indexed-gpu"],
+       "moments": p.VARIANTS["indexed-gpu-moments"]}
 
 
 def _params(S, name):
@@ -25,7 +26,7 @@ def _params(S, name):
     return params_ns(D=D, omega=om, m0=m0, z1=z1, coeff=c)
 
 
-@pytest.mark.parametrize("arith", ["exact", "fast"])
+@pytest.mark.parametrize("arith", ["exact", "fast", "moments"])
 def test_sweep_vs_reference_golden(arith):
     S = golden("sweeps.npz")
     for name in S["names"]:
@@ -36,7 +37,7 @@ def test_sweep_vs_reference_golden(arith):
         assert ea <= TOL[arith] and eb <= TOL[arith], (name, ea, eb)
 
 
-@pytest.mark.parametrize("arith", ["exact", "fast"])
+@pytest.mark.parametrize("arith", ["exact", "fast", "moments"])
 @pytest.mark.parametrize("tag", ["c0", "ragged", "sub256", "c2"])
 def test_sweep_vs_oracle_random_states(arith, tag):
     g = golden_grid(tag)
@@ -62,36 +63,38 @@ def test_search_and_indexed_bitwise_equal_and_deterministic():
         assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
 
 
+@pytest.mark.parametrize("arith", [p.Arithmetic.FAST, p.Arithmetic.MOMENTS])
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_row_sharded_sweepers_assemble_bitwise(world):
+def test_row_sharded_sweepers_assemble_bitwise(world, arith):
     """Rows owned by rank r of W (r, r+W, ...) reproduce the full sweep bitwise:
     a row's reduction never depends on which sweeper/GPU computes it."""
     g = golden_grid("default")
     rng = np.random.default_rng(2)
     a, b = rng.uniform(1, 2, g.n_ext), rng.uniform(0, 1, g.n_ext)
     prm = params_ns()
-    full = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX).sweep(a, b)
+    full = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, arith).sweep(a, b)
     ao, bo = np.full(g.n_ext, np.nan), np.full(g.n_ext, np.nan)
     for r in range(world):
-        sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, rows=(r, world))
+        sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, arith, rows=(r, world))
         x, y = sw.sweep(a, b)
         ao[r::world], bo[r::world] = x[r::world], y[r::world]
         sw.close()
     assert np.array_equal(ao, full[0]) and np.array_equal(bo, full[1])
 
 
-def test_free_theory_and_chiral_limit():
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu-moments"])
+def test_free_theory_and_chiral_limit(vname):
     g = golden_grid("small")
     free = params_ns(D=0.0, m0=0.01)
-    a, b = p.iterate_once(g, np.full(g.n_ext, 1.7), np.full(g.n_ext, 0.2), free, p.VARIANTS["indexed-gpu-exact"])
+    a, b = p.iterate_once(g, np.full(g.n_ext, 1.7), np.full(g.n_ext, 0.2), free, p.VARIANTS[vname])
     assert np.all(a == 1.0) and np.all(b == 0.01)
     a, b = np.full(g.n_ext, 1.3), np.zeros(g.n_ext)
     for _ in range(10):
-        a, b = p.iterate_once(g, a, b, params_ns(), p.VARIANTS["indexed-gpu-exact"])
+        a, b = p.iterate_once(g, a, b, params_ns(), p.VARIANTS[vname])
         assert np.all(b == 0.0)
 
 
-@pytest.mark.parametrize("arith", ["exact", "fast"])
+@pytest.mark.parametrize("arith", ["exact", "fast", "moments"])
 def test_numerical_failure_location(arith):
     E = golden("errors.npz")
     g = golden_grid("small")
