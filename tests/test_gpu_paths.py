@@ -61,3 +61,15 @@ def test_layouts_bitwise_equal(n, m, k):
     ae, be, _ = _sweep(g, prm, {}, p.Arithmetic.EXACT)
     assert np.max(np.abs(a0 - ae) / np.abs(ae)) < 1e-12
     assert np.max(np.abs(b0 - be)) / np.max(np.abs(be)) < 1e-12
+
+
+@pytest.mark.parametrize("n,m,k", [(128, 128, 64), (300, 1000, 16)])
+def test_moments_warps_per_row_bitwise_equal(n, m, k):
+    """The moments kernel's warps per row (DSE_MOM_WPR) changes which warp
+    sums which group of radial nodes, never the order: bit-identical."""
+    g = p.build_grid(n, m, k, 1e-4, 1e4)
+    prm = p.ModelParams(N=n, m_rad=m, m_ang=k, xi=1e-10)
+    ref = _sweep(g, prm, {}, p.Arithmetic.MOMENTS)
+    for wpr in ("1", "2", "4", "8", "3"):
+        x = _sweep(g, prm, {"DSE_MOM_WPR": wpr}, p.Arithmetic.MOMENTS)
+        assert np.array_equal(ref[0], x[0]) and np.array_equal(ref[1], x[1]), wpr
