@@ -144,6 +144,19 @@ def device_info(device: int = 0):
     return name.value.decode(), sms.value
 
 
+_SWEEP_RAW = []
+
+
+def sweep_raw():
+    """dse_sweeper_sweep bound with raw integer addresses (no pointer objects
+    per call): the prototype of include/dse_b200.h with void* arguments."""
+    if not _SWEEP_RAW:
+        vp = ctypes.c_void_p
+        fn = ctypes.CFUNCTYPE(ctypes.c_int, vp, vp, vp, vp, vp, vp)(("dse_sweeper_sweep", load()))
+        _SWEEP_RAW.append(fn)
+    return _SWEEP_RAW[0]
+
+
 def as_f64(a):
     a = np.ascontiguousarray(a, dtype=np.float64)
     return a, a.ctypes.data_as(f64p)

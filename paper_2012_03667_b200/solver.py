@@ -162,16 +162,22 @@ def resolve_threads(variant: AlgorithmVariant) -> int:
     return n
 
 
+_TORCH_CUDA = []  # [torch.cuda] once it is known to be importable and available (checked once per process)
+
+
 def _device() -> int:
     env = os.environ.get(DEVICE_ENV_VAR)
     if env:
         return int(env)
-    try:
-        import torch  # optional: follow the caller's current device when torch is in use
-        if torch.cuda.is_available() and torch.cuda.is_initialized():
-            return torch.cuda.current_device()
-    except Exception:  # noqa: BLE001
-        pass
+    if not _TORCH_CUDA:
+        try:
+            import torch  # optional: follow the caller's current device when torch is in use
+            _TORCH_CUDA.append(torch.cuda if torch.cuda.is_available() else None)
+        except Exception:  # noqa: BLE001
+            _TORCH_CUDA.append(None)
+    tc = _TORCH_CUDA[0]
+    if tc is not None and tc.is_initialized():
+        return tc.current_device()
     return int(os.environ.get("LOCAL_RANK", "0"))
 
 
@@ -212,14 +218,14 @@ class GpuSweeper:
         self._lock = threading.Lock()
 
     def sweep(self, a, b):
-        a, pa = nat.as_f64(a)
-        b, pb = nat.as_f64(b)
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
         ao = np.empty(self.n)
         bo = np.empty(self.n)
         err = nat.DseErr()
-        with self._lock:
-            rc = self.lib.dse_sweeper_sweep(self.handle, pa, pb, ao.ctypes.data_as(nat.f64p),
-                                            bo.ctypes.data_as(nat.f64p), ctypes.byref(err))
+        with self._lock:  # raw addresses: the per-call hot path (iterate_once)
+            rc = nat.sweep_raw()(self.handle, a.ctypes.data, b.ctypes.data, ao.ctypes.data, bo.ctypes.data,
+                                 ctypes.byref(err))
         nat.raise_for(rc, err)
         return ao, bo
 
