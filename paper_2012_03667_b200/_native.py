@@ -48,6 +48,17 @@ class DseLayout(ctypes.Structure):
                                               "split_rows", "node_chunk")]
 
 
+class DseMuGrid(ctypes.Structure):
+    _fields_ = [(n, f64p) for n in ("p_ext", "ps2_ext", "p4_ext", "q_int", "qs2_int", "q4_int", "meas_s", "meas_4",
+                                    "z_nodes", "z_weights")] + \
+               [("brk_s", i64p), ("brk_4", i64p)] + [(n, ctypes.c_int64) for n in ("n_s", "n_4", "m_s", "m_4", "m_ang")]
+
+
+class DseMuParams(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("coeff", "omega", "m0", "z1", "mu", "xi", "relaxation")] + \
+               [("max_iterations", ctypes.c_int64), ("vertex", ctypes.c_int64)]
+
+
 _LIB = None
 
 # (name, restype, argtypes) -- one row per declaration in include/dse_b200.h
@@ -94,6 +105,19 @@ _PROTOS = [
     ("dse_plan_info", ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, i32p, i32p, ctypes.c_int64, i32p, i32p, i32p,
                                      ctypes.c_int64, i64p, i64p]),
     ("dse_debug_check_flags", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32)]),
+    ("dse_mu_sweeper_create", ctypes.c_int, [ctypes.POINTER(DseMuGrid), ctypes.POINTER(DseMuParams), ctypes.c_int,
+                                             ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p),
+                                             ctypes.POINTER(DseErr)]),
+    ("dse_mu_sweeper_destroy", ctypes.c_int, [ctypes.c_void_p]),
+    ("dse_mu_solve", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DseMuParams), f64p, f64p, f64p, i64p,
+                                    ctypes.POINTER(ctypes.c_int), f64p, ctypes.POINTER(DseErr)]),
+    ("dse_mu_sweep", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DseMuParams), f64p, f64p, f64p, f64p, f64p, f64p,
+                                    ctypes.POINTER(DseErr)]),
+    ("dse_mu_solve_load", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_size_t, ctypes.POINTER(DseErr)]),
+    ("dse_mu_solve_resume", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
+    ("dse_mu_interp", ctypes.c_int, [ctypes.c_void_p, f64p, f64p, ctypes.POINTER(DseErr)]),
+    ("dse_mu_sweeper_stats", ctypes.c_int, [ctypes.c_void_p, i64p, i64p, i32p, i64p]),
     ("dse_launch_count", ctypes.c_int64, []),
 ]
 

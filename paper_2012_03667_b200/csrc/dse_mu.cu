@@ -1,0 +1,794 @@
+// dse_mu.cu -- finite chemical potential sweep (BASELINE configs 3-4).
+// Included at the end of dse_b200.cu (one translation unit: it reuses the
+// fast exp, the reciprocal, the error helpers and the launch counter).
+//
+// The reference has no finite-mu path; this is
+// the self-derived extension written out in DESIGN.md "Finite chemical
+// potential" and restated independently by oracle/mu_oracle.py (explicit
+// 4-vector components, pinned against explicit Dirac traces and, at mu = 0,
+// pointwise against the reference's integrand_terms, kernels.py:152-175).
+//
+// Per external point p~ = (|p|, p4 + i mu) and internal node q~ = (|q|,
+// q4 + i mu) every projection of T_mu_nu(k) gamma_mu S(q~) Gamma_nu is a
+// polynomial of degree <= 2 in r = p.q (spatial) and <= 1 in K = 1/k^2
+// (DESIGN.md derives the coefficients).  With the interaction g(k^2) K and
+// the angular weights, the angular sum of a (row, node) pair therefore
+// factors into five real moments
+//     S0 = sum_k w e K,  S1 = sum_k w e K r,  T0 = sum_k w e K^2,
+//     T1 = sum_k w e K^2 r,  T2 = sum_k w e K^2 r^2      (e = exp(-k^2/w^2))
+// accumulated point by point (one exp and one reciprocal per point), then
+// contracted once per pair with complex coefficients.  Every point is still
+// evaluated every iteration (the "integrand points" metric); the pair-level
+// contraction is ~1/32 of the work at m_ang = 32.
+//
+// Layout: state X[2][3][n_ext] complex (ping-pong by iteration parity),
+// node table NB[m_int] = {A_q, B_q, C_q, 1/den_q} rebuilt every iteration by
+// bilinear interpolation (bitwise the oracle's op order), per-CTA delta
+// maxima (max is exact, so any order gives the same stop decision).  One
+// cooperative persistent launch runs the whole loop: interpolate | grid
+// barrier | sweep rows | grid barrier | stop test.  Each row is reduced by one
+// CTA of 256 threads in a fixed order: results are bitwise independent of
+// the grid size and of row sharding.
+
+namespace mu {
+
+struct cplx {
+    double x, y;
+};
+__device__ __forceinline__ cplx C(double x, double y) { return cplx{x, y}; }
+__device__ __forceinline__ cplx operator+(cplx a, cplx b) { return C(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cplx operator-(cplx a, cplx b) { return C(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ cplx operator*(cplx a, cplx b) { return C(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)); }
+__device__ __forceinline__ cplx operator*(double s, cplx a) { return C(s * a.x, s * a.y); }
+__device__ __forceinline__ cplx rcp(cplx a) {
+    // 1/a with a scale so that |a|^2 neither overflows nor underflows
+    const double s = fmax(fabs(a.x), fabs(a.y));
+    const double is = 1.0 / s;
+    const double ax = a.x * is, ay = a.y * is;
+    const double d = 1.0 / fma(ax, ax, ay * ay);
+    return C(ax * d * is, -ay * d * is);
+}
+// a*x + y for complex a, real x, complex y
+__device__ __forceinline__ cplx cfma(cplx a, double x, cplx y) { return C(fma(a.x, x, y.x), fma(a.y, x, y.y)); }
+
+struct MuArgs {
+    const double *P, *P2, *p4, *Qs, *Q2, *q4, *meas_s, *meas_4, *z, *wz, *exp_tbl;
+    const int *brk_s, *brk_4;
+    int n_s, n_4, m_s, m_4, K;
+    int row_start, row_stride, n_rows;  // owned external points: row_start + r*row_stride
+    double coeff, w2, exp_c1, skip_k2, mu, z1, m0z1, xi, relax;
+    double2* X;            // [2][3][n_ext]
+    double2* NB;           // [m_int][4]: A_q, B_q, C_q, 1/den
+    double* bmax;          // [gridDim][3]
+    unsigned* ctr;         // [2] row tickets
+    unsigned long long* err;  // [2] lowest failing row
+    long long* status;     // [0] iterations done, [1] converged, [2] failed iteration, [3] failing row
+    double* hist;          // (cap+1) x 4 or null
+    long long* evaluated;  // pairs evaluated (diagnostic; null = not counted)
+    int it_begin, it_end, sweep_only, vertex;
+};
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// clamped linear rule of the reference along one axis (interpolation.py:71-72, :125-132)
+__device__ __forceinline__ double axis_lin(bool in, double x0, double x1, double v0, double v1, double q) {
+    return in ? dse::lin_eval(x0, x1, v0, v1, q) : v0;
+}
+
+__device__ void interp_node(const MuArgs& a, const double2* __restrict__ F, int js, int j4, double2& out) {
+    const int n_s = a.n_s, n_4 = a.n_4;
+    const int is = a.brk_s[js], i4 = a.brk_4[j4];
+    const int slo = min(max(is, 0), n_s - 1), shi = min(max(is + 1, 0), n_s - 1);
+    const int tlo = min(max(i4, 0), n_4 - 1), thi = min(max(i4 + 1, 0), n_4 - 1);
+    const bool sin_ = is >= 0 && is < n_s - 1, tin = i4 >= 0 && i4 < n_4 - 1;
+    const double xs0 = a.P2[slo], xs1 = a.P2[shi], qs = a.Q2[js];
+    const double x40 = a.p4[tlo], x41 = a.p4[thi], q4 = a.q4[j4];
+    const double2 v00 = F[slo * n_4 + tlo], v10 = F[shi * n_4 + tlo];
+    const double2 v01 = F[slo * n_4 + thi], v11 = F[shi * n_4 + thi];
+    const double f0x = axis_lin(sin_, xs0, xs1, v00.x, v10.x, qs), f1x = axis_lin(sin_, xs0, xs1, v01.x, v11.x, qs);
+    const double f0y = axis_lin(sin_, xs0, xs1, v00.y, v10.y, qs), f1y = axis_lin(sin_, xs0, xs1, v01.y, v11.y, qs);
+    out.x = axis_lin(tin, x40, x41, f0x, f1x, q4);
+    out.y = axis_lin(tin, x40, x41, f0y, f1y, q4);
+}
+
+// Phase I: dressing values and 1/den at every internal node
+__device__ void build_nodes(const MuArgs& a, const double2* __restrict__ Xin) {
+    const int n_ext = a.n_s * a.n_4, m_int = a.m_s * a.m_4;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m_int; j += gridDim.x * blockDim.x) {
+        const int js = j / a.m_4, j4 = j - js * a.m_4;
+        double2 v[3];
+        for (int f = 0; f < 3; ++f) interp_node(a, Xin + f * n_ext, js, j4, v[f]);
+        const cplx Aq = C(v[0].x, v[0].y), Bq = C(v[1].x, v[1].y), Cq = C(v[2].x, v[2].y);
+        const cplx q4t = C(a.q4[j4], a.mu);
+        const cplx den = a.Q2[js] * (Aq * Aq) + (q4t * q4t) * (Cq * Cq) + Bq * Bq;
+        cplx r = rcp(den);
+        // a non-finite node poisons 1/den so that no pair using it is skipped
+        // (the oracle's 0 * NaN = NaN flags it at every angle)
+        if (!isfinite(v[0].x + v[0].y + v[1].x + v[1].y + v[2].x + v[2].y + r.x + r.y)) r = C(NAN, NAN);
+        double2* o = a.NB + 4 * (size_t)j;
+        o[0] = v[0];
+        o[1] = v[1];
+        o[2] = v[2];
+        o[3] = make_double2(r.x, r.y);
+    }
+}
+
+struct RowC {
+    double P, P2, p4r;
+    cplx p4t, Ap, Bp, Cp;
+};
+
+// One (row, node) pair: angular moments, then the complex contraction.
+// acc[0..5] += (A, B, C channel) * meas * coeff / den (before the row's
+// division by |p|^2 and p~4).
+template <int V, bool kNoSkip = false>
+__device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, int j, const double2* __restrict__ zw,
+                                             unsigned tbl, double acc[6], bool& evaluated) {
+    const int js = j / a.m_4, j4 = j - js * a.m_4;
+    const double Qs = __ldg(a.Qs + js), Q2 = __ldg(a.Q2 + js), q4r = __ldg(a.q4 + j4);
+    const double k4 = q4r - rc.p4r;
+    const double dPQ = rc.P - Qs;
+    const double2* nb = a.NB + 4 * (size_t)j;
+    const double2 vR = nb[3];
+    // exp(-k^2/w^2) underflows at every angle: an exact-zero pair,
+    // unless the node is non-finite (then the oracle's 0 * NaN is NaN too)
+    evaluated = kNoSkip || fma(dPQ, dPQ, k4 * k4) <= a.skip_k2 || !isfinite(vR.x);
+    if (!evaluated) return;
+    const double PQ = rc.P * Qs;
+    const double c0 = fma(k4, k4, rc.P2 + Q2);
+    const dse::ExpK ek{a.exp_c1, 0.0};
+    double S0 = 0.0, S1 = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < a.K; ++k) {
+        const double2 zk = zw[k];
+        const double r = PQ * zk.x;
+        const double k2 = fma(-2.0, r, c0);
+        const double K = dse::rcp_nr(k2);
+        const double e = zk.y * dse::exp_neg_k2(k2, ek, tbl);
+        const double eK = e * K;
+        S0 += eK;
+        S1 = fma(eK, r, S1);
+        const double eKK = eK * K;
+        T0 += eKK;
+        const double t = eKK * r;
+        T1 += t;
+        T2 = fma(t, r, T2);
+    }
+    const double2 vA = nb[0], vB = nb[1], vC = nb[2];
+    const cplx Aq = C(vA.x, vA.y), Bq = C(vB.x, vB.y), Cq = C(vC.x, vC.y);
+    const cplx q4t = C(q4r, a.mu);
+    const cplx t4 = C(q4r + rc.p4r, 2.0 * a.mu);
+    const double P2 = rc.P2;
+    const double kts = Q2 - P2;
+    // q~^2 - p~^2 = k.t (complex), real part as (Q2 - P2) + k4 (q4 + p4)
+    const cplx kt = C(fma(k4, q4r + rc.p4r, kts), 2.0 * a.mu * k4);
+    const cplx rkt = rcp(kt);
+    const cplx sA = 0.5 * (rc.Ap + Aq), sC = 0.5 * (rc.Cp + Cq);
+    const cplx dA = (Aq - rc.Ap) * rkt, dC = (Cq - rc.Cp) * rkt, dB = (Bq - rc.Bp) * rkt;
+    const cplx tau0 = 2.0 * sA + sC;
+    const cplx tau1 = (k4 * k4) * (sA - sC);
+    const cplx Cq_q4t = Cq * q4t;
+    const cplx akQ = Q2 * Aq + k4 * Cq_q4t;                       // k.Q = akQ - Aq r
+    const cplx akQp = Q2 * (sA * Aq) + k4 * (sC * Cq_q4t);        // k.Q' = akQp - sA Aq r
+    const cplx nu1 = Aq * dA;
+    const cplx Cq_q4t_t4 = Cq_q4t * t4;
+    const cplx nu0 = Q2 * nu1 + Cq_q4t_t4 * dC;                   // Q.D = nu0 + nu1 r
+    const cplx delta0 = (P2 + Q2) * dA + (t4 * t4) * dC;          // u.D = delta0 + 2 dA r - psi K
+    const cplx psi = (kts * dA + k4 * (dC * t4)) * kt;
+    const cplx eta0 = Q2 * Aq + Cq_q4t_t4;                        // Q.t = eta0 + Aq r
+    const cplx sAAq = sA * Aq;
+    // vertex structures by mode (DSE_MU_VERTEX_*): Sigma parts always, the
+    // Delta_A/Delta_C parts in the A/C channels (fac), in the B channel (fb),
+    // Delta_B in the B channel (fdb); V is a compile-time constant.
+    constexpr bool fac = V == DSE_MU_VERTEX_BC;
+    constexpr bool fb = V != DSE_MU_VERTEX_BC1;
+    constexpr bool fdb = V == DSE_MU_VERTEX_BC;
+    const cplx zero = C(0.0, 0.0);
+    // A channel (e = p_vec): F_A = cA00 + cA01 r + K (cA10 + cA11 r + cA12 r^2)
+    const cplx lam0 = akQp + sA * akQ;
+    const cplx cA00 = fac ? (-0.5 * P2) * (nu0 + dA * eta0) : zero;
+    cplx cA01 = Aq * tau0 - 2.0 * sAAq;
+    cplx cA10 = (-P2) * lam0;
+    cplx cA11 = lam0 + (2.0 * P2) * sAAq + Aq * tau1;
+    if (fac) {
+        cA01 = cA01 - 0.5 * (nu0 + P2 * nu1 - Aq * delta0 + dA * (eta0 + P2 * Aq));
+        cA10 = cA10 - (0.5 * P2) * (kt * (nu0 - dA * akQ));
+        cA11 = cA11 - 0.5 * (kt * (P2 * nu1 - nu0) + Aq * psi + (dA * kt) * (P2 * Aq - akQ));
+    }
+    const cplx cA12 = -2.0 * sAAq;
+    // C channel (e = unit 4): F_C = cC00 + cC01 r + K (cC10 + cC11 r)
+    const cplx lam0c = akQp + sC * akQ;
+    const cplx lam1c = (sA + sC) * Aq;
+    const cplx dCt4 = dC * t4;
+    cplx cC00 = Cq_q4t * (tau0 - 2.0 * sC);
+    cplx cC01 = zero;
+    cplx cC10 = k4 * lam0c + Cq_q4t * tau1;
+    cplx cC11 = (-k4) * lam1c;
+    if (fac) {
+        cC00 = cC00 - 0.5 * (t4 * nu0 - Cq_q4t * delta0 + dCt4 * eta0);
+        cC01 = -0.5 * (t4 * nu1 - 2.0 * (Cq_q4t * dA) + dCt4 * Aq);
+        cC10 = cC10 - 0.5 * (Cq_q4t * psi - kt * (k4 * nu0 + dCt4 * akQ));
+        cC11 = cC11 - 0.5 * (kt * (dCt4 * Aq - k4 * nu1));
+    }
+    // B channel: F_B = cB00 + cB01 r + K (cB10 + cB11 r)
+    cplx cB00 = Bq * tau0, cB01 = zero, cB10 = Bq * tau1, cB11 = zero;
+    if (fb) {
+        cB00 = cB00 + Bq * (0.5 * delta0);
+        cB01 = Bq * dA;
+        cB10 = cB10 - Bq * (0.5 * psi);
+    }
+    if (fdb) {
+        cB00 = cB00 - dB * eta0;
+        cB01 = cB01 - dB * Aq;
+        cB10 = cB10 + dB * (kt * akQ);
+        cB11 = -1.0 * (dB * (kt * Aq));
+    }
+    // contract with the moments, scale by meas * coeff / den
+    const cplx FA = cfma(cA00, S0, cfma(cA01, S1, cfma(cA10, T0, cfma(cA11, T1, T2 * cA12))));
+    const cplx FC = cfma(cC00, S0, cfma(cC01, S1, cfma(cC10, T0, T1 * cC11)));
+    const cplx FB = cfma(cB00, S0, cfma(cB01, S1, cfma(cB10, T0, T1 * cB11)));
+    const double sc = a.coeff * (__ldg(a.meas_s + js) * __ldg(a.meas_4 + j4));
+    const cplx rd = sc * C(vR.x, vR.y);
+    const cplx gA = FA * rd, gB = FB * rd, gC = FC * rd;
+    acc[0] += gA.x; acc[1] += gA.y;
+    acc[2] += gB.x; acc[3] += gB.y;
+    acc[4] += gC.x; acc[5] += gC.y;
+}
+
+__device__ __forceinline__ double hyp(double x, double y) { return hypot(x, y); }
+
+template <int V>
+__global__ void __launch_bounds__(kThreads, 1) mu_solve_kernel(MuArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double smem[];
+    double* etbl = smem;                                           // 2^bits
+    double2* zw = reinterpret_cast<double2*>(smem + (1 << dse::kExpTableBits));  // K
+    double* red = smem + (1 << dse::kExpTableBits) + 2 * a.K;      // kWarps * 6
+    __shared__ unsigned s_row;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < (1 << dse::kExpTableBits); i += kThreads) etbl[i] = __ldg(a.exp_tbl + i);
+    for (int k = tid; k < a.K; k += kThreads) zw[k] = make_double2(__ldg(a.z + k), __ldg(a.wz + k));
+    __syncthreads();
+    const unsigned tbl = dse::smem_addr(etbl);
+    const int n_ext = a.n_s * a.n_4, m_int = a.m_s * a.m_4;
+    long long it_done = a.it_begin;
+    bool converged = false;
+    for (int it = a.it_begin; it < a.it_end; ++it) {
+        const int cur = it & 1;
+        const double2* Xin = a.X + (size_t)cur * 3 * n_ext;
+        double2* Xout = a.X + (size_t)(cur ^ 1) * 3 * n_ext;
+        if (blockIdx.x == 0 && tid == 0) {
+            a.ctr[cur ^ 1] = 0u;
+            a.err[cur ^ 1] = ~0ull;
+        }
+        build_nodes(a, Xin);
+        grid.sync();
+        // ---- phase S: rows by ticket, one CTA per row ----
+        double dmax[3] = {0.0, 0.0, 0.0};
+        long long pairs = 0;
+        for (;;) {
+            if (tid == 0) s_row = atomicAdd(a.ctr + cur, 1u);
+            __syncthreads();
+            const unsigned r = s_row;
+            __syncthreads();
+            if (r >= (unsigned)a.n_rows) break;
+            const int i = a.row_start + (int)r * a.row_stride;
+            const int is = i / a.n_4, i4 = i - is * a.n_4;
+            RowC rc;
+            rc.P = a.P[is];
+            rc.P2 = a.P2[is];
+            rc.p4r = a.p4[i4];
+            rc.p4t = C(rc.p4r, a.mu);
+            const double2 va = Xin[i], vb = Xin[n_ext + i], vc = Xin[2 * n_ext + i];
+            rc.Ap = C(va.x, va.y);
+            rc.Bp = C(vb.x, vb.y);
+            rc.Cp = C(vc.x, vc.y);
+            double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int j = tid; j < m_int; j += kThreads) {
+                bool ev;
+                pair_contrib<V>(a, rc, j, zw, tbl, acc, ev);
+                pairs += ev;
+            }
+            // fixed-order block reduction
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                double v = acc[c];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) red[warp * 6 + c] = v;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double s[6];
+                for (int c = 0; c < 6; ++c) {
+                    double v = red[c];
+                    for (int w = 1; w < kWarps; ++w) v += red[w * 6 + c];
+                    s[c] = v;
+                }
+                // A' = z1 + sum_A / |p|^2 ; B' = m0 z1 + sum_B ; C' = z1 + sum_C / p~4
+                double2 An = make_double2(a.z1 + s[0] / rc.P2, s[1] / rc.P2);
+                double2 Bn = make_double2(a.m0z1 + s[2], s[3]);
+                const cplx cn = C(s[4], s[5]) * rcp(rc.p4t);
+                double2 Cn = make_double2(a.z1 + cn.x, cn.y);
+                if (a.relax != 1.0) {
+                    const double om = 1.0 - a.relax;
+                    An = make_double2(a.relax * An.x + om * va.x, a.relax * An.y + om * va.y);
+                    Bn = make_double2(a.relax * Bn.x + om * vb.x, a.relax * Bn.y + om * vb.y);
+                    Cn = make_double2(a.relax * Cn.x + om * vc.x, a.relax * Cn.y + om * vc.y);
+                }
+                const bool fin = isfinite(An.x) && isfinite(An.y) && isfinite(Bn.x) && isfinite(Bn.y) &&
+                                 isfinite(Cn.x) && isfinite(Cn.y);
+                if (!fin) atomicMin(a.err + cur, (unsigned long long)i);
+                Xout[i] = An;
+                Xout[n_ext + i] = Bn;
+                Xout[2 * n_ext + i] = Cn;
+                dmax[0] = fmax(dmax[0], hyp(An.x - va.x, An.y - va.y));
+                dmax[1] = fmax(dmax[1], hyp(Bn.x - vb.x, Bn.y - vb.y));
+                dmax[2] = fmax(dmax[2], hyp(Cn.x - vc.x, Cn.y - vc.y));
+            }
+        }
+        if (tid == 0) {
+            a.bmax[3 * blockIdx.x + 0] = dmax[0];
+            a.bmax[3 * blockIdx.x + 1] = dmax[1];
+            a.bmax[3 * blockIdx.x + 2] = dmax[2];
+        }
+        if (a.evaluated) {
+            for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+            if (lane == 0 && it == a.it_begin) atomicAdd((unsigned long long*)a.evaluated, (unsigned long long)pairs);
+        }
+        grid.sync();
+        // ---- stop test (every CTA, identical decision) ----
+        it_done = it + 1;
+        if (a.err[cur] != ~0ull) {
+            if (blockIdx.x == 0 && tid == 0) {
+                a.status[2] = it + 1;
+                a.status[3] = (long long)a.err[cur];
+            }
+            break;
+        }
+        double d[3] = {0.0, 0.0, 0.0};
+        for (int b = 0; b < (int)gridDim.x; ++b)
+            for (int c = 0; c < 3; ++c) d[c] = fmax(d[c], a.bmax[3 * b + c]);
+        if (blockIdx.x == 0 && tid == 0 && a.hist) {
+            double* h = a.hist + 4 * (size_t)(it + 1);
+            h[0] = double(it + 1);
+            h[1] = d[0];
+            h[2] = d[1];
+            h[3] = d[2];
+        }
+        if (!a.sweep_only && d[0] < a.xi && d[1] < a.xi && d[2] < a.xi) {
+            converged = true;
+            break;
+        }
+        // the next iteration's tickets/err slots were reset before this
+        // iteration's first barrier; bmax is rewritten only after the next
+        // barrier, so it is safe to fall through
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        a.status[0] = it_done;
+        a.status[1] = converged ? 1 : 0;
+    }
+}
+
+// Failure location: first non-finite point (j, k) in row-major order of the
+// failing row, evaluated with the same pair form.  One thread per node.
+template <int V>
+__global__ void __launch_bounds__(kThreads) mu_locate_kernel(MuArgs a, int i, int in_buf, unsigned long long* first) {
+    __shared__ double etbl[1 << dse::kExpTableBits];
+    for (int t = threadIdx.x; t < (1 << dse::kExpTableBits); t += blockDim.x) etbl[t] = __ldg(a.exp_tbl + t);
+    __syncthreads();
+    const unsigned tbl = dse::smem_addr(etbl);
+    const int n_ext = a.n_s * a.n_4, m_int = a.m_s * a.m_4;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m_int) return;
+    const double2* Xin = a.X + (size_t)in_buf * 3 * n_ext;
+    const int is = i / a.n_4, i4 = i - is * a.n_4;
+    RowC rc;
+    rc.P = a.P[is];
+    rc.P2 = a.P2[is];
+    rc.p4r = a.p4[i4];
+    rc.p4t = C(rc.p4r, a.mu);
+    rc.Ap = C(Xin[i].x, Xin[i].y);
+    rc.Bp = C(Xin[n_ext + i].x, Xin[n_ext + i].y);
+    rc.Cp = C(Xin[2 * n_ext + i].x, Xin[2 * n_ext + i].y);
+    // per point: run the pair form with a single-angle weight table
+    double2 zw1[1];
+    MuArgs b = a;
+    b.K = 1;
+    for (int k = 0; k < a.K; ++k) {
+        zw1[0] = make_double2(a.z[k], a.wz[k]);
+        double acc[6] = {0, 0, 0, 0, 0, 0};
+        bool ev;
+        pair_contrib<V, true>(b, rc, j, zw1, tbl, acc, ev);
+        bool bad = false;
+        for (int c = 0; c < 6; ++c) bad |= !isfinite(acc[c]);
+        if (bad) {
+            atomicMin(first, (unsigned long long)j * (unsigned long long)a.K + (unsigned long long)k);
+            return;
+        }
+    }
+}
+
+__global__ void mu_reset_kernel(unsigned* ctr, unsigned long long* err, long long* status) {
+    const int t = threadIdx.x;
+    if (t < 2) {
+        ctr[t] = 0u;
+        err[t] = ~0ull;
+    }
+    if (t < 4) status[t] = 0;
+}
+
+}  // namespace mu
+
+struct dse_mu_sweeper {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int n_s = 0, n_4 = 0, m_s = 0, m_4 = 0, K = 0;
+    int row_start = 0, row_stride = 1, n_rows = 0;
+    dse_mu_params prm{};
+    double *d_P = nullptr, *d_P2 = nullptr, *d_p4 = nullptr, *d_Qs = nullptr, *d_Q2 = nullptr, *d_q4 = nullptr;
+    double *d_ms = nullptr, *d_m4 = nullptr, *d_z = nullptr, *d_wz = nullptr, *d_etbl = nullptr;
+    int *d_brk_s = nullptr, *d_brk_4 = nullptr;
+    double2* d_X = nullptr;
+    double2* d_NB = nullptr;
+    double* d_bmax = nullptr;
+    unsigned* d_ctr = nullptr;
+    unsigned long long* d_err = nullptr;
+    long long* d_status = nullptr;
+    long long* d_eval = nullptr;
+    double* d_hist = nullptr;
+    size_t hist_cap = 0;
+    int blocks = 0;
+    size_t smem = 0;
+    long long it_next = 0;
+    long long evaluated_pairs = -1;
+};
+
+namespace {
+
+int mu_check_params(const dse_mu_params* p, dse_err* err) {
+    if (!(p->omega > 0.0) || !(p->coeff >= 0.0) || !(p->xi > 0.0) || !(p->relaxation > 0.0 && p->relaxation <= 1.0) ||
+        p->max_iterations < 1 || !(p->mu >= 0.0) || !std::isfinite(p->mu) || p->vertex < 0 || p->vertex > 2)
+        return fail(err, DSE_EPARAM, "finite-mu parameters out of range");
+    return DSE_OK;
+}
+
+mu::MuArgs mu_make_args(dse_mu_sweeper* s, const dse_mu_params& p, int it_begin, int it_end, bool hist, bool sweep_only,
+                        bool count) {
+    mu::MuArgs a{};
+    a.P = s->d_P; a.P2 = s->d_P2; a.p4 = s->d_p4; a.Qs = s->d_Qs; a.Q2 = s->d_Q2; a.q4 = s->d_q4;
+    a.meas_s = s->d_ms; a.meas_4 = s->d_m4; a.z = s->d_z; a.wz = s->d_wz; a.exp_tbl = s->d_etbl;
+    a.brk_s = s->d_brk_s; a.brk_4 = s->d_brk_4;
+    a.n_s = s->n_s; a.n_4 = s->n_4; a.m_s = s->m_s; a.m_4 = s->m_4; a.K = s->K;
+    a.row_start = s->row_start; a.row_stride = s->row_stride; a.n_rows = s->n_rows;
+    a.coeff = p.coeff;
+    a.w2 = p.omega * p.omega;
+    a.exp_c1 = -double(1 << dse::kExpTableBits) * 1.4426950408889634 / a.w2;
+    a.skip_k2 = 708.0 * a.w2;  // exp(-x) < 2^-1021 beyond: the point is an exact zero of the sum (F8)
+    a.mu = p.mu; a.z1 = p.z1; a.m0z1 = p.m0 * p.z1; a.xi = p.xi; a.relax = p.relaxation;
+    a.X = s->d_X; a.NB = s->d_NB; a.bmax = s->d_bmax; a.ctr = s->d_ctr; a.err = s->d_err; a.status = s->d_status;
+    a.hist = hist ? s->d_hist : nullptr;
+    a.evaluated = count ? s->d_eval : nullptr;
+    a.it_begin = it_begin; a.it_end = it_end; a.sweep_only = sweep_only ? 1 : 0;
+    a.vertex = (int)p.vertex;
+    return a;
+}
+
+const void* mu_kernel_ptr(int v) {
+    if (v == DSE_MU_VERTEX_BC1) return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BC1>;
+    if (v == DSE_MU_VERTEX_BCB) return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BCB>;
+    return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BC>;
+}
+
+int mu_launch(dse_mu_sweeper* s, const mu::MuArgs& a, bool reset, dse_err* err) {
+    if (reset) {
+        mu::mu_reset_kernel<<<1, 32, 0, s->stream>>>(s->d_ctr, s->d_err, s->d_status);
+        CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(1);
+    }
+    mu::MuArgs b = a;
+    void* args[] = {&b};
+    CUDA_TRY(cudaLaunchCooperativeKernel(mu_kernel_ptr(a.vertex), dim3(s->blocks), dim3(mu::kThreads), args,
+                                         s->smem, s->stream));
+    g_launches.fetch_add(1);
+    return DSE_OK;
+}
+
+int mu_failure(dse_mu_sweeper* s, const dse_mu_params& p, long long it_fail, long long row, dse_err* err) {
+    // locate the first non-finite point of the failing row on the input state of that iteration
+    unsigned long long* d_first = nullptr;
+    CUDA_TRY(cudaMalloc(&d_first, sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(d_first, 0xff, sizeof(unsigned long long), s->stream));
+    mu::MuArgs a = mu_make_args(s, p, 0, 0, false, true, false);
+    const int m_int = s->m_s * s->m_4;
+    // the node table NB still holds the failing iteration's input (the loop stops right after it)
+    const int in_buf = (int)((it_fail - 1) & 1);
+    auto loc = p.vertex == DSE_MU_VERTEX_BC1 ? mu::mu_locate_kernel<DSE_MU_VERTEX_BC1>
+             : p.vertex == DSE_MU_VERTEX_BCB ? mu::mu_locate_kernel<DSE_MU_VERTEX_BCB>
+                                             : mu::mu_locate_kernel<DSE_MU_VERTEX_BC>;
+    loc<<<(m_int + mu::kThreads - 1) / mu::kThreads, mu::kThreads, 0, s->stream>>>(a, (int)row, in_buf,
+                                                                                                  d_first);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    unsigned long long first = ~0ull;
+    CUDA_TRY(cudaMemcpyAsync(&first, d_first, sizeof(first), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    cudaFree(d_first);
+    long long j = -1, k = -1;
+    if (first != ~0ull) {
+        j = (long long)(first / (unsigned long long)s->K);
+        k = (long long)(first % (unsigned long long)s->K);
+    }
+    fail(err, DSE_ENUMERIC, "non-finite integrand in finite-mu sweep at row=%lld, radial=%lld, angular=%lld", row, j, k);
+    if (err) {
+        err->iteration = it_fail;
+        err->row = row;
+        err->radial = j;
+        err->angular = k;
+    }
+    return DSE_ENUMERIC;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dse_mu_sweeper_create(const dse_mu_grid* g, const dse_mu_params* p, int device, int64_t row_start,
+                          int64_t row_stride, dse_mu_sweeper** out, dse_err* err) {
+    ok(err);
+    if (!g || !p || !out) return fail(err, DSE_EPARAM, "null argument");
+    *out = nullptr;
+    if (g->n_s < 2 || g->n_4 < 2 || g->m_s < 2 || g->m_4 < 2 || g->m_ang < 1)
+        return fail(err, DSE_EPARAM, "finite-mu grid sizes out of range");
+    if (g->n_s * g->n_4 > (1LL << 30) || g->m_s * g->m_4 > (1LL << 30) || g->m_ang > 4096)
+        return fail(err, DSE_EPARAM, "finite-mu grid too large");
+    if (!g->p_ext || !g->ps2_ext || !g->p4_ext || !g->q_int || !g->qs2_int || !g->q4_int || !g->meas_s ||
+        !g->meas_4 || !g->z_nodes || !g->z_weights || !g->brk_s || !g->brk_4)
+        return fail(err, DSE_EPARAM, "null grid array");
+    int rc = mu_check_params(p, err);
+    if (rc) return rc;
+    const int64_t n_ext = g->n_s * g->n_4;
+    if (row_stride < 1 || row_start < 0 || (row_start >= n_ext && n_ext > 0))
+        return fail(err, DSE_EPARAM, "bad row partition start=%lld stride=%lld", (long long)row_start,
+                    (long long)row_stride);
+    for (int64_t j = 0; j < g->m_s; ++j)
+        if (g->brk_s[j] < -1 || g->brk_s[j] > g->n_s - 1) return fail(err, DSE_EPARAM, "brk_s out of range");
+    for (int64_t j = 0; j < g->m_4; ++j)
+        if (g->brk_4[j] < -1 || g->brk_4[j] > g->n_4 - 1) return fail(err, DSE_EPARAM, "brk_4 out of range");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(err, DSE_EENV, "CUDA device %d not present", device);
+    CUDA_TRY(cudaSetDevice(device));
+    auto* s = new dse_mu_sweeper();
+    s->device = device;
+    s->n_s = (int)g->n_s; s->n_4 = (int)g->n_4; s->m_s = (int)g->m_s; s->m_4 = (int)g->m_4; s->K = (int)g->m_ang;
+    s->row_start = (int)row_start; s->row_stride = (int)row_stride;
+    s->n_rows = (int)((n_ext - row_start + row_stride - 1) / row_stride);
+    s->prm = *p;
+    auto bail = [&](int code) {
+        dse_mu_sweeper_destroy(s);
+        return code;
+    };
+#define MU_TRY(expr)                                                                                       \
+    do {                                                                                                   \
+        cudaError_t _e = (expr);                                                                           \
+        if (_e != cudaSuccess)                                                                             \
+            return bail(fail(err, DSE_EENV, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__)); \
+    } while (0)
+    MU_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    cudaStream_t st = s->stream;
+    std::vector<int> bs(g->brk_s, g->brk_s + g->m_s), b4(g->brk_4, g->brk_4 + g->m_4);
+    MU_TRY(upload(&s->d_P, g->p_ext, g->n_s, st));
+    MU_TRY(upload(&s->d_P2, g->ps2_ext, g->n_s, st));
+    MU_TRY(upload(&s->d_p4, g->p4_ext, g->n_4, st));
+    MU_TRY(upload(&s->d_Qs, g->q_int, g->m_s, st));
+    MU_TRY(upload(&s->d_Q2, g->qs2_int, g->m_s, st));
+    MU_TRY(upload(&s->d_q4, g->q4_int, g->m_4, st));
+    MU_TRY(upload(&s->d_ms, g->meas_s, g->m_s, st));
+    MU_TRY(upload(&s->d_m4, g->meas_4, g->m_4, st));
+    MU_TRY(upload(&s->d_z, g->z_nodes, g->m_ang, st));
+    MU_TRY(upload(&s->d_wz, g->z_weights, g->m_ang, st));
+    MU_TRY(upload(&s->d_brk_s, bs.data(), bs.size(), st));
+    MU_TRY(upload(&s->d_brk_4, b4.data(), b4.size(), st));
+    std::vector<double> etbl(1 << dse::kExpTableBits);
+    for (int i = 0; i < (1 << dse::kExpTableBits); ++i) etbl[i] = std::exp2(i / double(1 << dse::kExpTableBits));
+    MU_TRY(upload(&s->d_etbl, etbl.data(), etbl.size(), st));
+    MU_TRY(cudaMalloc(&s->d_X, sizeof(double2) * 2 * 3 * (size_t)n_ext));
+    MU_TRY(cudaMemsetAsync(s->d_X, 0, sizeof(double2) * 2 * 3 * (size_t)n_ext, st));
+    MU_TRY(cudaMalloc(&s->d_NB, sizeof(double2) * 4 * (size_t)(g->m_s * g->m_4)));
+    MU_TRY(cudaMalloc(&s->d_ctr, 2 * sizeof(unsigned)));
+    MU_TRY(cudaMalloc(&s->d_err, 2 * sizeof(unsigned long long)));
+    MU_TRY(cudaMalloc(&s->d_status, 4 * sizeof(long long)));
+    MU_TRY(cudaMalloc(&s->d_eval, sizeof(long long)));
+    s->smem = (size_t)((1 << dse::kExpTableBits) + 2 * s->K + mu::kWarps * 6) * sizeof(double);
+    int per_sm = 1 << 30, sms = 0;
+    for (int v : {DSE_MU_VERTEX_BC, DSE_MU_VERTEX_BC1, DSE_MU_VERTEX_BCB}) {
+        MU_TRY(cudaFuncSetAttribute(mu_kernel_ptr(v), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
+        int n = 0;
+        MU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mu_kernel_ptr(v), mu::kThreads, s->smem));
+        per_sm = std::min(per_sm, n);
+    }
+    MU_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    if (per_sm < 1) return bail(fail(err, DSE_EENV, "finite-mu kernel does not fit on an SM"));
+    s->blocks = per_sm * sms;
+    if (const char* e = getenv("DSE_MU_BLOCKS")) s->blocks = std::max(1, std::min(s->blocks, atoi(e)));
+    MU_TRY(cudaMalloc(&s->d_bmax, 3 * sizeof(double) * (size_t)s->blocks));
+    MU_TRY(cudaStreamSynchronize(st));
+#undef MU_TRY
+    *out = s;
+    return DSE_OK;
+}
+
+int dse_mu_sweeper_destroy(dse_mu_sweeper* s) {
+    if (!s) return DSE_OK;
+    cudaSetDevice(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    for (void* p : {(void*)s->d_P, (void*)s->d_P2, (void*)s->d_p4, (void*)s->d_Qs, (void*)s->d_Q2, (void*)s->d_q4,
+                    (void*)s->d_ms, (void*)s->d_m4, (void*)s->d_z, (void*)s->d_wz, (void*)s->d_etbl,
+                    (void*)s->d_brk_s, (void*)s->d_brk_4, (void*)s->d_X, (void*)s->d_NB, (void*)s->d_bmax,
+                    (void*)s->d_ctr, (void*)s->d_err, (void*)s->d_status, (void*)s->d_eval, (void*)s->d_hist})
+        if (p) cudaFree(p);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+    return DSE_OK;
+}
+
+// Upload a complex state (host, interleaved re/im, n_ext each) into X[0].
+static int mu_put_state(dse_mu_sweeper* s, const double* A, const double* B, const double* C_, dse_err* err) {
+    const size_t n = (size_t)s->n_s * s->n_4;
+    const double* src[3] = {A, B, C_};
+    for (int f = 0; f < 3; ++f)
+        CUDA_TRY(cudaMemcpyAsync(s->d_X + f * n, src[f], n * sizeof(double2), cudaMemcpyHostToDevice, s->stream));
+    return DSE_OK;
+}
+
+int dse_mu_solve(dse_mu_sweeper* s, const dse_mu_params* params, double* A, double* B, double* C_,
+                 int64_t* iterations, int* converged, double* history, dse_err* err) {
+    ok(err);
+    if (!s || !A || !B || !C_) return fail(err, DSE_EPARAM, "null argument");
+    const dse_mu_params p = params ? *params : s->prm;
+    int rc = mu_check_params(&p, err);
+    if (rc) return rc;
+    if (s->row_start != 0 || s->row_stride != 1)
+        return fail(err, DSE_EPARAM, "dse_mu_solve needs a sweeper that owns every row");
+    CUDA_TRY(cudaSetDevice(s->device));
+    const size_t cap = (size_t)p.max_iterations;
+    if (history && s->hist_cap < cap + 1) {
+        if (s->d_hist) cudaFree(s->d_hist);
+        s->d_hist = nullptr;
+        CUDA_TRY(cudaMalloc(&s->d_hist, 4 * sizeof(double) * (cap + 1)));
+        s->hist_cap = cap + 1;
+    }
+    rc = mu_put_state(s, A, B, C_, err);
+    if (rc) return rc;
+    const bool count = s->evaluated_pairs < 0;
+    if (count) CUDA_TRY(cudaMemsetAsync(s->d_eval, 0, sizeof(long long), s->stream));
+    mu::MuArgs a = mu_make_args(s, p, 0, (int)cap, history != nullptr, false, count);
+    rc = mu_launch(s, a, true, err);
+    if (rc) return rc;
+    long long st[4];
+    CUDA_TRY(cudaMemcpyAsync(st, s->d_status, sizeof(st), cudaMemcpyDeviceToHost, s->stream));
+    long long ev = 0;
+    if (count) CUDA_TRY(cudaMemcpyAsync(&ev, s->d_eval, sizeof(ev), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (count) s->evaluated_pairs = ev;
+    if (st[2] != 0) return mu_failure(s, p, st[2], st[3], err);
+    const long long n = st[0];
+    const size_t ne = (size_t)s->n_s * s->n_4;
+    const double2* fin = s->d_X + (size_t)(n & 1) * 3 * ne;
+    double* dst[3] = {A, B, C_};
+    for (int f = 0; f < 3; ++f)
+        CUDA_TRY(cudaMemcpyAsync(dst[f], fin + f * ne, ne * sizeof(double2), cudaMemcpyDeviceToHost, s->stream));
+    if (history) {
+        CUDA_TRY(cudaMemcpyAsync(history + 4, s->d_hist + 4, 4 * sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost,
+                                 s->stream));
+        history[0] = 0.0;
+        history[1] = history[2] = history[3] = NAN;
+    }
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (iterations) *iterations = n;
+    if (converged) *converged = (int)st[1];
+    return DSE_OK;
+}
+
+int dse_mu_sweep(dse_mu_sweeper* s, const dse_mu_params* params, const double* A, const double* B, const double* C_,
+                 double* A_out, double* B_out, double* C_out, dse_err* err) {
+    ok(err);
+    if (!s || !A || !B || !C_ || !A_out || !B_out || !C_out) return fail(err, DSE_EPARAM, "null argument");
+    dse_mu_params p = params ? *params : s->prm;
+    int rc = mu_check_params(&p, err);
+    if (rc) return rc;
+    p.relaxation = 1.0;  // one Jacobi sweep (iterate_once, solver.py:201-212)
+    CUDA_TRY(cudaSetDevice(s->device));
+    rc = mu_put_state(s, A, B, C_, err);
+    if (rc) return rc;
+    const size_t ne = (size_t)s->n_s * s->n_4;
+    // rows not owned keep their input value in the output buffer
+    CUDA_TRY(cudaMemcpyAsync(s->d_X + 3 * ne, s->d_X, 3 * ne * sizeof(double2), cudaMemcpyDeviceToDevice, s->stream));
+    mu::MuArgs a = mu_make_args(s, p, 0, 1, false, true, false);
+    rc = mu_launch(s, a, true, err);
+    if (rc) return rc;
+    long long st[4];
+    CUDA_TRY(cudaMemcpyAsync(st, s->d_status, sizeof(st), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (st[2] != 0) {
+        rc = mu_failure(s, p, st[2], st[3], err);
+        if (err) err->iteration = 0;
+        return rc;
+    }
+    double* dst[3] = {A_out, B_out, C_out};
+    for (int f = 0; f < 3; ++f)
+        CUDA_TRY(cudaMemcpyAsync(dst[f], s->d_X + (3 + f) * ne, ne * sizeof(double2), cudaMemcpyDeviceToHost,
+                                 s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return DSE_OK;
+}
+
+int dse_mu_solve_load(dse_mu_sweeper* s, const double* dA, const double* dB, const double* dC, uintptr_t stream,
+                      dse_err* err) {
+    ok(err);
+    if (!s || !dA || !dB || !dC) return fail(err, DSE_EPARAM, "null argument");
+    CUDA_TRY(cudaSetDevice(s->device));
+    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    const size_t ne = (size_t)s->n_s * s->n_4;
+    const double* src[3] = {dA, dB, dC};
+    for (int f = 0; f < 3; ++f)
+        CUDA_TRY(cudaMemcpyAsync(s->d_X + f * ne, src[f], ne * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    mu::mu_reset_kernel<<<1, 32, 0, st>>>(s->d_ctr, s->d_err, s->d_status);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    s->it_next = 0;
+    if (stream) CUDA_TRY(cudaStreamSynchronize(st));
+    return DSE_OK;
+}
+
+int dse_mu_solve_resume(dse_mu_sweeper* s, int64_t n_iterations, uintptr_t stream, dse_err* err) {
+    ok(err);
+    if (!s || n_iterations < 1) return fail(err, DSE_EPARAM, "bad argument");
+    CUDA_TRY(cudaSetDevice(s->device));
+    cudaStream_t keep = s->stream;
+    if (stream) s->stream = (cudaStream_t)stream;
+    mu::MuArgs a = mu_make_args(s, s->prm, (int)s->it_next, (int)(s->it_next + n_iterations), false, true, false);
+    int rc = mu_launch(s, a, false, err);
+    s->stream = keep;
+    if (rc) return rc;
+    s->it_next += n_iterations;
+    return DSE_OK;
+}
+
+int dse_mu_interp(dse_mu_sweeper* s, const double* F, double* out, dse_err* err) {
+    ok(err);
+    if (!s || !F || !out) return fail(err, DSE_EPARAM, "null argument");
+    CUDA_TRY(cudaSetDevice(s->device));
+    const size_t ne = (size_t)s->n_s * s->n_4, m = (size_t)s->m_s * s->m_4;
+    int rc = mu_put_state(s, F, F, F, err);
+    if (rc) return rc;
+    // one sweep-only launch with zero iterations does not build nodes; run the
+    // node phase through a 1-iteration sweep on a copy and read NB[.][0]
+    mu::MuArgs a = mu_make_args(s, s->prm, 0, 1, false, true, false);
+    rc = mu_launch(s, a, true, err);
+    if (rc) return rc;
+    std::vector<double2> nb(4 * m);
+    CUDA_TRY(cudaMemcpyAsync(nb.data(), s->d_NB, nb.size() * sizeof(double2), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    for (size_t j = 0; j < m; ++j) {
+        out[2 * j] = nb[4 * j].x;
+        out[2 * j + 1] = nb[4 * j].y;
+    }
+    (void)ne;
+    return DSE_OK;
+}
+
+int dse_mu_sweeper_stats(dse_mu_sweeper* s, int64_t* nominal_points, int64_t* evaluated_points, int32_t* blocks,
+                         int64_t* smem_bytes) {
+    if (!s) return DSE_EPARAM;
+    const int64_t pairs = (int64_t)s->n_rows * s->m_s * s->m_4;
+    if (nominal_points) *nominal_points = pairs * s->K;
+    if (evaluated_points) *evaluated_points = s->evaluated_pairs < 0 ? -1 : s->evaluated_pairs * s->K;
+    if (blocks) *blocks = s->blocks;
+    if (smem_bytes) *smem_bytes = (int64_t)s->smem;
+    return DSE_OK;
+}
+
+}  // extern "C"

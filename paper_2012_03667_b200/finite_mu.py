@@ -1,0 +1,210 @@
+"""Finite chemical potential solves on the GPU (BASELINE configs 3-4).
+
+The reference has no finite-mu path:
+this module extends the drop-in's vacuum API (solve / iterate_once /
+solve_batch, solver.py:201-266) to the complex dressing functions A, B, C of
+S^-1(p~) = i gamma.p A + i gamma_4 p~4 C + B on the 2-D external grid
+(|p|, p4 + i mu) of mu_grid.py, with the same conventions: a Jacobi sweep,
+the optional relaxation blend (solver.py:249-251), the max-norm stop rule
+all(d < xi) over |dA|, |dB|, |dC| (iteration.py:34-38), cap -> converged=False
+(iteration.py:40), the error classes of errors.py.
+
+Everything numeric runs in libdse_b200.so (dse_mu_* in include/dse_b200.h):
+the whole loop is one cooperative kernel launch per solve.  There is no CPU
+fallback.  The equations are in DESIGN.md "Finite chemical potential"; the CPU
+oracle (test infrastructure only) is oracle/mu_oracle.py.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _native as nat
+from .mu_grid import VERTICES, MuGrid, MuParams, build_mu_grid, grid_for
+
+__all__ = ["MuIterationRecord", "MuSolution", "MuSweeper", "solve_mu", "iterate_mu_once", "solve_mu_batch",
+           "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
+
+
+@dataclass(frozen=True)
+class MuIterationRecord:
+    n: int
+    delta_a: float
+    delta_b: float
+    delta_c: float
+
+
+@dataclass
+class MuSolution:
+    A: np.ndarray            # complex (n_s, n_4)
+    B: np.ndarray
+    C: np.ndarray
+    iterations: int
+    converged: bool
+    history: list = field(repr=False)
+    grid: MuGrid = field(repr=False)
+    params: MuParams = field(repr=False)
+
+    @property
+    def mass(self) -> np.ndarray:
+        """M = B / A (complex), the mass function on the external grid."""
+        return self.B / self.A
+
+
+def _c_params(p: MuParams) -> nat.DseMuParams:
+    return nat.DseMuParams(coeff=p.interaction_coeff, omega=p.omega, m0=p.m0, z1=p.z1, mu=p.mu, xi=p.xi,
+                           relaxation=p.relaxation, max_iterations=int(p.max_iterations),
+                           vertex=VERTICES.index(p.vertex))
+
+
+def _state(x, shape, default) -> np.ndarray:
+    if x is None:
+        return np.full(shape, default, dtype=np.complex128)
+    a = np.array(x, dtype=np.complex128).reshape(shape)
+    return np.ascontiguousarray(a)
+
+
+def _ptr(a: np.ndarray):
+    return a.view(np.float64).ctypes.data_as(nat.f64p)
+
+
+class MuSweeper:
+    """Device-resident finite-mu grid + state buffers (dse_mu_sweeper_*).
+    rows row_start + r*row_stride are owned (multi-GPU sharding)."""
+
+    def __init__(self, grid: MuGrid, params: MuParams, device: int = 0, row_start: int = 0, row_stride: int = 1):
+        params.validate()
+        self.grid, self.params, self.device = grid, params, device
+        lib = nat.load()
+        self._keep = [np.ascontiguousarray(getattr(grid, n), dtype=np.float64) for n in
+                      ("p_ext", "ps2_ext", "p4_ext", "q_int", "qs2_int", "q4_int", "meas_s", "meas_4", "z_nodes",
+                       "z_weights")]
+        bs = np.ascontiguousarray(grid.brk_s, dtype=np.int64)
+        b4 = np.ascontiguousarray(grid.brk_4, dtype=np.int64)
+        self._keep += [bs, b4]
+        g = nat.DseMuGrid(*[a.ctypes.data_as(nat.f64p) for a in self._keep[:10]], bs.ctypes.data_as(nat.i64p),
+                          b4.ctypes.data_as(nat.i64p), grid.n_s, grid.n_4, grid.m_s, grid.m_4, grid.m_ang)
+        cp = _c_params(params)
+        h = ctypes.c_void_p()
+        err = nat.DseErr()
+        nat.raise_for(lib.dse_mu_sweeper_create(ctypes.byref(g), ctypes.byref(cp), device, row_start, row_stride,
+                                                ctypes.byref(h), ctypes.byref(err)), err)
+        self._h = h
+        self._lib = lib
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.dse_mu_sweeper_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def solve(self, params: MuParams | None = None, a0=None, b0=None, c0=None, history: bool = True) -> MuSolution:
+        p = self.params if params is None else params
+        p.validate()
+        shape = (self.grid.n_s, self.grid.n_4)
+        A, B, C = _state(a0, shape, 1.0), _state(b0, shape, 0.3), _state(c0, shape, 1.0)
+        hist = np.full((p.max_iterations + 1, 4), np.nan) if history else None
+        it = ctypes.c_int64()
+        conv = ctypes.c_int()
+        err = nat.DseErr()
+        cp = _c_params(p)
+        rc = self._lib.dse_mu_solve(self._h, ctypes.byref(cp), _ptr(A), _ptr(B), _ptr(C), ctypes.byref(it),
+                                    ctypes.byref(conv), hist.ctypes.data_as(nat.f64p) if hist is not None else None,
+                                    ctypes.byref(err))
+        nat.raise_for(rc, err)
+        n = int(it.value)
+        records = []
+        if hist is not None:
+            records = [MuIterationRecord(0, float("nan"), float("nan"), float("nan"))]
+            records += [MuIterationRecord(int(r[0]), float(r[1]), float(r[2]), float(r[3])) for r in hist[1:n + 1]]
+        return MuSolution(A=A, B=B, C=C, iterations=n, converged=bool(conv.value), history=records, grid=self.grid,
+                          params=p)
+
+    def sweep(self, A, B, C, params: MuParams | None = None):
+        p = self.params if params is None else params
+        shape = (self.grid.n_s, self.grid.n_4)
+        A, B, C = _state(A, shape, 0), _state(B, shape, 0), _state(C, shape, 0)
+        outs = [np.empty(shape, np.complex128) for _ in range(3)]
+        err = nat.DseErr()
+        cp = _c_params(p)
+        rc = self._lib.dse_mu_sweep(self._h, ctypes.byref(cp), _ptr(A), _ptr(B), _ptr(C), *[_ptr(o) for o in outs],
+                                    ctypes.byref(err))
+        nat.raise_for(rc, err)
+        return tuple(outs)
+
+    def interp(self, F) -> np.ndarray:
+        shape = (self.grid.n_s, self.grid.n_4)
+        F = _state(F, shape, 0)
+        out = np.empty((self.grid.m_s, self.grid.m_4), np.complex128)
+        err = nat.DseErr()
+        nat.raise_for(self._lib.dse_mu_interp(self._h, _ptr(F), _ptr(out), ctypes.byref(err)), err)
+        return out
+
+    def stats(self) -> dict:
+        nom, ev, sm = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        blocks = ctypes.c_int32()
+        self._lib.dse_mu_sweeper_stats(self._h, ctypes.byref(nom), ctypes.byref(ev), ctypes.byref(blocks),
+                                       ctypes.byref(sm))
+        return dict(nominal_points=nom.value, evaluated_points=ev.value, blocks=blocks.value, smem_bytes=sm.value)
+
+
+def solve_mu(params: MuParams | None = None, grid: MuGrid | None = None, a0=None, b0=None, c0=None,
+             device: int = 0) -> MuSolution:
+    """Finite-mu analogue of solve (solver.py:221-266): A = C = 1, B = 0.3
+    GeV by default (BASELINE config 3's initial guess)."""
+    params = MuParams() if params is None else params
+    params.validate()
+    grid = grid_for(params) if grid is None else grid
+    with MuSweeper(grid, params, device) as sw:
+        return sw.solve(params, a0, b0, c0)
+
+
+def iterate_mu_once(grid: MuGrid, A, B, C, params: MuParams, device: int = 0):
+    """One Jacobi sweep (iterate_once, solver.py:201-212) -> (A', B', C')."""
+    with MuSweeper(grid, params, device) as sw:
+        return sw.sweep(A, B, C, params)
+
+
+def solve_mu_batch(mus, params: MuParams | None = None, grid: MuGrid | None = None, device: int = 0,
+                   history: bool = False) -> list:
+    """Independent solves at each chemical potential in `mus` on one grid
+    (BASELINE config 4: replicas, no exchange): the grid is uploaded once
+    and every solve is one on-device loop."""
+    params = MuParams() if params is None else params
+    grid = grid_for(params) if grid is None else grid
+    out = []
+    with MuSweeper(grid, params, device) as sw:
+        for m in mus:
+            out.append(sw.solve(replace(params, mu=float(m)), history=history))
+    return out
+
+
+def interp_mu(grid: MuGrid, F, params: MuParams | None = None, device: int = 0) -> np.ndarray:
+    """The sweep's complex 2-D interpolation of F at every internal node."""
+    params = MuParams() if params is None else params
+    with MuSweeper(grid, params, device) as sw:
+        return sw.interp(F)
+
+
+def default_grid(params: MuParams | None = None) -> MuGrid:
+    return grid_for(MuParams() if params is None else params)
+
+
+_ = build_mu_grid  # re-exported

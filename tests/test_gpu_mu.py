@@ -1,0 +1,142 @@
+"""GPU: the finite-mu path (BASELINE configs 3-4) through the C ABI against
+the CPU oracle oracle/mu_oracle.py.  Parity is to the self-derived oracle:
+there is no reference implementation ("parity unpinned").
+
+Tolerances: interpolation bitwise (same op order); one sweep 1e-11 hybrid
+(SURVEY §8c measure; the kernel contracts angular moments per pair, a
+different summation order); a converged solve 1e-9 hybrid with the same
+iteration count (north_star)."""
+import os
+
+import numpy as np
+import pytest
+
+import mu_oracle
+from conftest import hybrid_rel
+from paper_2012_03667_b200 import NumericalFailureError
+from paper_2012_03667_b200.finite_mu import MuSweeper, iterate_mu_once, solve_mu, solve_mu_batch
+from paper_2012_03667_b200.mu_grid import MuParams, grid_for
+
+pytestmark = pytest.mark.gpu
+
+SMALL = dict(n_s=10, n_4=12, m_s=14, m_4=16, m_ang=6)
+
+
+def _state(g, seed):
+    rng = np.random.default_rng(seed)
+    shape = (g.n_s, g.n_4)
+    A = 1.0 + 0.8 * rng.random(shape) + 0.1j * rng.standard_normal(shape)
+    B = 0.1 + 0.5 * rng.random(shape) + 0.05j * rng.standard_normal(shape)
+    C = 1.0 + 0.8 * rng.random(shape) + 0.1j * rng.standard_normal(shape)
+    return A, B, C
+
+
+def _cmp(x, ref):
+    return max(hybrid_rel(np.real(x), np.real(ref)), hybrid_rel(np.imag(x), np.imag(ref)))
+
+
+def test_interp_bitwise():
+    p = MuParams(**SMALL)
+    g = grid_for(p)
+    A, _, _ = _state(g, 1)
+    with MuSweeper(g, p) as sw:
+        out = sw.interp(A)
+    ref = mu_oracle.interp2d(g, A)
+    assert np.array_equal(out.view(np.float64), ref.view(np.float64))
+
+
+@pytest.mark.parametrize("vertex", ["bc", "bc1", "bcb"])
+@pytest.mark.parametrize("mu", [0.0, 0.2])
+def test_sweep_matches_oracle(vertex, mu):
+    p = MuParams(mu=mu, vertex=vertex, **SMALL)
+    g = grid_for(p)
+    A, B, C = _state(g, 2)
+    got = iterate_mu_once(g, A, B, C, p)
+    ref = mu_oracle.sweep(g, p, A, B, C)
+    for x, r in zip(got, ref):
+        assert _cmp(x, r) < 1e-11
+
+
+def test_sweep_row_sharding_and_grid_size_bitwise():
+    p = MuParams(**SMALL)
+    g = grid_for(p)
+    A, B, C = _state(g, 3)
+    with MuSweeper(g, p) as sw:
+        full = sw.sweep(A, B, C)
+    W = 3
+    stitched = [np.zeros_like(full[0]) for _ in range(3)]
+    for r in range(W):
+        with MuSweeper(g, p, row_start=r, row_stride=W) as sw:
+            part = sw.sweep(A, B, C)
+        for f in range(3):
+            stitched[f].reshape(-1)[r::W] = part[f].reshape(-1)[r::W]
+    for f in range(3):
+        assert np.array_equal(stitched[f].view(np.float64), full[f].view(np.float64))
+    os.environ["DSE_MU_BLOCKS"] = "5"
+    try:
+        with MuSweeper(g, p) as sw:
+            few = sw.sweep(A, B, C)
+    finally:
+        del os.environ["DSE_MU_BLOCKS"]
+    for f in range(3):
+        assert np.array_equal(few[f].view(np.float64), full[f].view(np.float64))
+
+
+@pytest.mark.parametrize("vertex", ["bcb", "bc1"])
+def test_solve_matches_oracle_iterations_and_values(vertex):
+    p = MuParams(mu=0.2, vertex=vertex, max_iterations=200, **SMALL)
+    g = grid_for(p)
+    A, B, C, n, conv, hist = mu_oracle.solve(g, p)
+    sol = solve_mu(p, g)
+    assert conv and sol.converged
+    assert sol.iterations == n
+    assert _cmp(sol.A, A) < 1e-9 and _cmp(sol.B, B) < 1e-9 and _cmp(sol.C, C) < 1e-9
+    assert len(sol.history) == len(hist)
+    for rec, h in zip(sol.history[1:], hist[1:]):
+        assert rec.n == h[0]
+        for got, ref in ((rec.delta_a, h[1]), (rec.delta_b, h[2]), (rec.delta_c, h[3])):
+            assert abs(got - ref) <= 1e-6 * ref + 1e-14
+
+
+def test_cap_is_not_an_error_and_relaxation():
+    p = MuParams(mu=0.1, vertex="bc1", max_iterations=3, relaxation=0.7, **SMALL)
+    g = grid_for(p)
+    A, B, C, n, conv, _ = mu_oracle.solve(g, p)
+    sol = solve_mu(p, g)
+    assert (sol.iterations, sol.converged) == (n, conv) == (3, False)
+    # three sweeps compound the per-sweep 1e-11 bound
+    assert _cmp(sol.A, A) < 1e-10 and _cmp(sol.B, B) < 1e-10 and _cmp(sol.C, C) < 1e-10
+
+
+def test_batch_equals_standalone():
+    p = MuParams(vertex="bc1", max_iterations=100, **SMALL)
+    g = grid_for(p)
+    mus = [0.05, 0.3]
+    batch = solve_mu_batch(mus, p, g)
+    for m, sol in zip(mus, batch):
+        one = solve_mu(MuParams(**{**p.__dict__, "mu": m}), g)
+        assert sol.iterations == one.iterations
+        assert np.array_equal(sol.A.view(np.float64), one.A.view(np.float64))
+
+
+def test_failure_location_matches_oracle():
+    p = MuParams(**SMALL)
+    g = grid_for(p)
+    A, B, C = _state(g, 4)
+    A[3, 5] = np.nan
+    with pytest.raises(mu_oracle.MuNumericalFailure) as ref:
+        mu_oracle.sweep(g, p, A, B, C)
+    with pytest.raises(NumericalFailureError) as got:
+        iterate_mu_once(g, A, B, C, p)
+    assert (got.value.row, got.value.radial, got.value.angular) == (ref.value.row, ref.value.radial,
+                                                                      ref.value.angular)
+
+
+def test_stats_count_points():
+    p = MuParams(vertex="bc1", max_iterations=2, **SMALL)
+    g = grid_for(p)
+    with MuSweeper(g, p) as sw:
+        sw.solve(p)
+        st = sw.stats()
+    assert st["nominal_points"] == g.nominal_points
+    assert 0 < st["evaluated_points"] <= st["nominal_points"]
