@@ -30,6 +30,8 @@
 // CTA of 256 threads in a fixed order: results are bitwise independent of
 // the grid size and of row sharding.
 
+#include <cub/block/block_scan.cuh>
+
 namespace mu {
 
 struct cplx {
@@ -62,6 +64,7 @@ struct MuArgs {
     double* bmax;          // [gridDim][3]
     unsigned* ctr;         // [2] row tickets
     unsigned long long* err;  // [2] lowest failing row
+    int* nonfinite;        // [2] some node value non-finite this iteration (no pair is skipped then)
     long long* status;     // [0] iterations done, [1] converged, [2] failed iteration, [3] failing row
     double* hist;          // (cap+1) x 4 or null
     long long* evaluated;  // pairs evaluated (diagnostic; null = not counted)
@@ -93,7 +96,7 @@ __device__ void interp_node(const MuArgs& a, const double2* __restrict__ F, int 
 }
 
 // Phase I: dressing values and 1/den at every internal node
-__device__ void build_nodes(const MuArgs& a, const double2* __restrict__ Xin) {
+__device__ void build_nodes(const MuArgs& a, const double2* __restrict__ Xin, int* flag) {
     const int n_ext = a.n_s * a.n_4, m_int = a.m_s * a.m_4;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m_int; j += gridDim.x * blockDim.x) {
         const int js = j / a.m_4, j4 = j - js * a.m_4;
@@ -105,7 +108,10 @@ __device__ void build_nodes(const MuArgs& a, const double2* __restrict__ Xin) {
         cplx r = rcp(den);
         // a non-finite node poisons 1/den so that no pair using it is skipped
         // (the oracle's 0 * NaN = NaN flags it at every angle)
-        if (!isfinite(v[0].x + v[0].y + v[1].x + v[1].y + v[2].x + v[2].y + r.x + r.y)) r = C(NAN, NAN);
+        if (!isfinite(v[0].x + v[0].y + v[1].x + v[1].y + v[2].x + v[2].y + r.x + r.y)) {
+            r = C(NAN, NAN);
+            atomicOr(flag, 1);
+        }
         double2* o = a.NB + 4 * (size_t)j;
         o[0] = v[0];
         o[1] = v[1];
@@ -122,19 +128,15 @@ struct RowC {
 // One (row, node) pair: angular moments, then the complex contraction.
 // acc[0..5] += (A, B, C channel) * meas * coeff / den (before the row's
 // division by |p|^2 and p~4).
-template <int V, bool kNoSkip = false>
-__device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, int j, const double2* __restrict__ zw,
-                                             unsigned tbl, double acc[6], bool& evaluated) {
-    const int js = j / a.m_4, j4 = j - js * a.m_4;
+template <int V>
+__device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, int js, int j4,
+                                             const double2* __restrict__ zw, unsigned tbl, double acc[6]) {
+    const int j = js * a.m_4 + j4;
     const double Qs = __ldg(a.Qs + js), Q2 = __ldg(a.Q2 + js), q4r = __ldg(a.q4 + j4);
     const double k4 = q4r - rc.p4r;
-    const double dPQ = rc.P - Qs;
+    // node values first: their latency hides behind the angular loop
     const double2* nb = a.NB + 4 * (size_t)j;
-    const double2 vR = nb[3];
-    // exp(-k^2/w^2) underflows at every angle: an exact-zero pair,
-    // unless the node is non-finite (then the oracle's 0 * NaN is NaN too)
-    evaluated = kNoSkip || fma(dPQ, dPQ, k4 * k4) <= a.skip_k2 || !isfinite(vR.x);
-    if (!evaluated) return;
+    const double2 vA = nb[0], vB = nb[1], vC = nb[2], vR = nb[3];
     const double PQ = rc.P * Qs;
     const double c0 = fma(k4, k4, rc.P2 + Q2);
     const dse::ExpK ek{a.exp_c1, 0.0};
@@ -155,7 +157,6 @@ __device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, in
         T1 += t;
         T2 = fma(t, r, T2);
     }
-    const double2 vA = nb[0], vB = nb[1], vC = nb[2];
     const cplx Aq = C(vA.x, vA.y), Bq = C(vB.x, vB.y), Cq = C(vC.x, vC.y);
     const cplx q4t = C(q4r, a.mu);
     const cplx t4 = C(q4r + rc.p4r, 2.0 * a.mu);
@@ -245,10 +246,15 @@ __global__ void __launch_bounds__(kThreads, 1) mu_solve_kernel(MuArgs a) {
     double* etbl = smem;                                           // 2^bits
     double2* zw = reinterpret_cast<double2*>(smem + (1 << dse::kExpTableBits));  // K
     double* red = smem + (1 << dse::kExpTableBits) + 2 * a.K;      // kWarps * 6
+    double* q4s = red + kWarps * 6;                                // m_4
+    int* rlo = reinterpret_cast<int*>(q4s + a.m_4);                // m_s: first evaluated j4 per js
+    int* roff = rlo + a.m_s;                                       // m_s + 1: flat offsets
     __shared__ unsigned s_row;
+    __shared__ int s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < (1 << dse::kExpTableBits); i += kThreads) etbl[i] = __ldg(a.exp_tbl + i);
     for (int k = tid; k < a.K; k += kThreads) zw[k] = make_double2(__ldg(a.z + k), __ldg(a.wz + k));
+    for (int k = tid; k < a.m_4; k += kThreads) q4s[k] = __ldg(a.q4 + k);
     __syncthreads();
     const unsigned tbl = dse::smem_addr(etbl);
     const int n_ext = a.n_s * a.n_4, m_int = a.m_s * a.m_4;
@@ -261,8 +267,9 @@ __global__ void __launch_bounds__(kThreads, 1) mu_solve_kernel(MuArgs a) {
         if (blockIdx.x == 0 && tid == 0) {
             a.ctr[cur ^ 1] = 0u;
             a.err[cur ^ 1] = ~0ull;
+            a.nonfinite[cur ^ 1] = 0;
         }
-        build_nodes(a, Xin);
+        build_nodes(a, Xin, a.nonfinite + cur);
         grid.sync();
         // ---- phase S: rows by ticket, one CTA per row ----
         double dmax[3] = {0.0, 0.0, 0.0};
@@ -284,12 +291,69 @@ __global__ void __launch_bounds__(kThreads, 1) mu_solve_kernel(MuArgs a) {
             rc.Ap = C(va.x, va.y);
             rc.Bp = C(vb.x, vb.y);
             rc.Cp = C(vc.x, vc.y);
-            double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            for (int j = tid; j < m_int; j += kThreads) {
-                bool ev;
-                pair_contrib<V>(a, rc, j, zw, tbl, acc, ev);
-                pairs += ev;
+            // Pairs whose exp(-k^2/w^2) underflows at every angle are exact
+            // zeros of the sum: per radial node js the evaluated q4
+            // form one window around p4.  Flatten the windows and deal the
+            // pairs round-robin, so every thread gets the same count.
+            const bool all = a.nonfinite[cur] != 0;  // a non-finite node must reach the sum
+            using Scan = cub::BlockScan<int, kThreads>;
+            __shared__ typename Scan::TempStorage scan_tmp;
+            if (tid == 0) s_carry = 0;
+            for (int base = 0; base < a.m_s; base += kThreads) {
+                const int js = base + tid;
+                int len = 0;
+                if (js < a.m_s) {
+                    int lo = 0, hi = a.m_4;
+                    if (!all) {
+                        const double dPQ = rc.P - __ldg(a.Qs + js);
+                        const double d2 = a.skip_k2 - dPQ * dPQ;
+                        if (d2 < 0.0) {
+                            hi = 0;
+                        } else {
+                            const double half = sqrt(d2) * (1.0 + 1e-12) + 1e-300;
+                            const double x0 = rc.p4r - half, x1 = rc.p4r + half;
+                            int l = 0, h = a.m_4;  // first q4 >= x0
+                            while (l < h) { const int m = (l + h) >> 1; if (q4s[m] < x0) l = m + 1; else h = m; }
+                            lo = l;
+                            h = a.m_4;             // first q4 > x1
+                            while (l < h) { const int m = (l + h) >> 1; if (q4s[m] <= x1) l = m + 1; else h = m; }
+                            hi = l;
+                        }
+                    }
+                    len = max(hi - lo, 0);
+                    rlo[js] = lo;
+                }
+                int ex;
+                __syncthreads();  // s_carry written
+                const int carry = s_carry;
+                Scan(scan_tmp).ExclusiveSum(len, ex);
+                if (js < a.m_s) roff[js] = carry + ex;
+                __syncthreads();
+                if (tid == kThreads - 1) s_carry = carry + ex + len;
             }
+            __syncthreads();
+            const int total = s_carry;
+            if (tid == 0) roff[a.m_s] = total;
+            __syncthreads();
+            double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            // the warp's lanes stay converged through the pair body: the node
+            // of flat index f is found by a fixed-trip binary search over the
+            // offsets (a data-dependent walk here split the warps, 6 of 32
+            // lanes active on average)
+            int top = 1;
+            while (top < a.m_s) top <<= 1;
+            for (int f0 = 0; f0 < total; f0 += kThreads) {
+                const int f = min(f0 + tid, total - 1);
+                int js = 0;
+                for (int step = top >> 1; step > 0; step >>= 1)
+                    js = (js + step < a.m_s && roff[js + step] <= f) ? js + step : js;
+                __syncwarp();
+                double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                pair_contrib<V>(a, rc, js, rlo[js] + (f - roff[js]), zw, tbl, part);
+                if (f0 + tid < total)
+                    for (int c = 0; c < 6; ++c) acc[c] += part[c];
+            }
+            pairs += (tid == 0) ? total : 0;
             // fixed-order block reduction
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
@@ -399,8 +463,7 @@ __global__ void __launch_bounds__(kThreads) mu_locate_kernel(MuArgs a, int i, in
     for (int k = 0; k < a.K; ++k) {
         zw1[0] = make_double2(a.z[k], a.wz[k]);
         double acc[6] = {0, 0, 0, 0, 0, 0};
-        bool ev;
-        pair_contrib<V, true>(b, rc, j, zw1, tbl, acc, ev);
+        pair_contrib<V>(b, rc, j / a.m_4, j % a.m_4, zw1, tbl, acc);
         bool bad = false;
         for (int c = 0; c < 6; ++c) bad |= !isfinite(acc[c]);
         if (bad) {
@@ -410,11 +473,12 @@ __global__ void __launch_bounds__(kThreads) mu_locate_kernel(MuArgs a, int i, in
     }
 }
 
-__global__ void mu_reset_kernel(unsigned* ctr, unsigned long long* err, long long* status) {
+__global__ void mu_reset_kernel(unsigned* ctr, unsigned long long* err, long long* status, int* nonfinite) {
     const int t = threadIdx.x;
     if (t < 2) {
         ctr[t] = 0u;
         err[t] = ~0ull;
+        nonfinite[t] = 0;
     }
     if (t < 4) status[t] = 0;
 }
@@ -437,6 +501,7 @@ struct dse_mu_sweeper {
     unsigned long long* d_err = nullptr;
     long long* d_status = nullptr;
     long long* d_eval = nullptr;
+    int* d_nonfinite = nullptr;
     double* d_hist = nullptr;
     size_t hist_cap = 0;
     int blocks = 0;
@@ -468,6 +533,7 @@ mu::MuArgs mu_make_args(dse_mu_sweeper* s, const dse_mu_params& p, int it_begin,
     a.skip_k2 = 708.0 * a.w2;  // exp(-x) < 2^-1021 beyond: the point is an exact zero of the sum (F8)
     a.mu = p.mu; a.z1 = p.z1; a.m0z1 = p.m0 * p.z1; a.xi = p.xi; a.relax = p.relaxation;
     a.X = s->d_X; a.NB = s->d_NB; a.bmax = s->d_bmax; a.ctr = s->d_ctr; a.err = s->d_err; a.status = s->d_status;
+    a.nonfinite = s->d_nonfinite;
     a.hist = hist ? s->d_hist : nullptr;
     a.evaluated = count ? s->d_eval : nullptr;
     a.it_begin = it_begin; a.it_end = it_end; a.sweep_only = sweep_only ? 1 : 0;
@@ -483,7 +549,7 @@ const void* mu_kernel_ptr(int v) {
 
 int mu_launch(dse_mu_sweeper* s, const mu::MuArgs& a, bool reset, dse_err* err) {
     if (reset) {
-        mu::mu_reset_kernel<<<1, 32, 0, s->stream>>>(s->d_ctr, s->d_err, s->d_status);
+        mu::mu_reset_kernel<<<1, 32, 0, s->stream>>>(s->d_ctr, s->d_err, s->d_status, s->d_nonfinite);
         CUDA_TRY(cudaGetLastError());
         g_launches.fetch_add(1);
     }
@@ -600,8 +666,10 @@ int dse_mu_sweeper_create(const dse_mu_grid* g, const dse_mu_params* p, int devi
     MU_TRY(cudaMalloc(&s->d_ctr, 2 * sizeof(unsigned)));
     MU_TRY(cudaMalloc(&s->d_err, 2 * sizeof(unsigned long long)));
     MU_TRY(cudaMalloc(&s->d_status, 4 * sizeof(long long)));
+    MU_TRY(cudaMalloc(&s->d_nonfinite, 2 * sizeof(int)));
     MU_TRY(cudaMalloc(&s->d_eval, sizeof(long long)));
-    s->smem = (size_t)((1 << dse::kExpTableBits) + 2 * s->K + mu::kWarps * 6) * sizeof(double);
+    s->smem = (size_t)((1 << dse::kExpTableBits) + 2 * s->K + mu::kWarps * 6 + s->m_4) * sizeof(double) +
+              (size_t)(2 * s->m_s + 2) * sizeof(int);
     int per_sm = 1 << 30, sms = 0;
     for (int v : {DSE_MU_VERTEX_BC, DSE_MU_VERTEX_BC1, DSE_MU_VERTEX_BCB}) {
         MU_TRY(cudaFuncSetAttribute(mu_kernel_ptr(v), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
@@ -627,7 +695,7 @@ int dse_mu_sweeper_destroy(dse_mu_sweeper* s) {
     for (void* p : {(void*)s->d_P, (void*)s->d_P2, (void*)s->d_p4, (void*)s->d_Qs, (void*)s->d_Q2, (void*)s->d_q4,
                     (void*)s->d_ms, (void*)s->d_m4, (void*)s->d_z, (void*)s->d_wz, (void*)s->d_etbl,
                     (void*)s->d_brk_s, (void*)s->d_brk_4, (void*)s->d_X, (void*)s->d_NB, (void*)s->d_bmax,
-                    (void*)s->d_ctr, (void*)s->d_err, (void*)s->d_status, (void*)s->d_eval, (void*)s->d_hist})
+                    (void*)s->d_ctr, (void*)s->d_err, (void*)s->d_status, (void*)s->d_eval, (void*)s->d_hist, (void*)s->d_nonfinite})
         if (p) cudaFree(p);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;
@@ -735,7 +803,7 @@ int dse_mu_solve_load(dse_mu_sweeper* s, const double* dA, const double* dB, con
     const double* src[3] = {dA, dB, dC};
     for (int f = 0; f < 3; ++f)
         CUDA_TRY(cudaMemcpyAsync(s->d_X + f * ne, src[f], ne * sizeof(double2), cudaMemcpyDeviceToDevice, st));
-    mu::mu_reset_kernel<<<1, 32, 0, st>>>(s->d_ctr, s->d_err, s->d_status);
+    mu::mu_reset_kernel<<<1, 32, 0, st>>>(s->d_ctr, s->d_err, s->d_status, s->d_nonfinite);
     CUDA_TRY(cudaGetLastError());
     g_launches.fetch_add(1);
     s->it_next = 0;

@@ -157,6 +157,16 @@ class MuSweeper:
         nat.raise_for(self._lib.dse_mu_interp(self._h, _ptr(F), _ptr(out), ctypes.byref(err)), err)
         return out
 
+    def load_device(self, dA: int, dB: int, dC: int, stream: int = 0) -> None:
+        """Device-resident state (complex, n_ext each, raw device addresses) as iteration 0."""
+        err = nat.DseErr()
+        nat.raise_for(self._lib.dse_mu_solve_load(self._h, dA, dB, dC, stream, ctypes.byref(err)), err)
+
+    def resume(self, n_iterations: int, stream: int = 0) -> None:
+        """Enqueue the next n_iterations of the on-device loop (no stop test, no sync)."""
+        err = nat.DseErr()
+        nat.raise_for(self._lib.dse_mu_solve_resume(self._h, n_iterations, stream, ctypes.byref(err)), err)
+
     def stats(self) -> dict:
         nom, ev, sm = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         blocks = ctypes.c_int32()
