@@ -227,6 +227,8 @@ def run_ours(args):
         extra["interp_config1"] = interp_bench(p, nat, torch, dev, peak_hbm())
     if not args.no_tts:
         extra["batched_scan"] = batch_bench(p)
+    if not args.no_mu:
+        extra["finite_mu"] = mu_bench(p, torch, dev, flush, args, peak, args.no_cpu)
     cpu = None
     if not args.no_cpu:
         rate, info = cpu_port_rate(grid, params, float(os.environ.get("BENCH_CPU_S", "10")),
@@ -460,6 +462,129 @@ def interp_bench(p, nat, torch, dev, hbm):
     return res
 
 
+# ncu SASS mix of mu_solve_kernel<bcb> (profiles/r01/SUMMARY.md): 2*DFMA + DMUL + DADD per evaluated point
+MU_FLOP_PER_POINT = 44.1
+
+
+def _mu_cpu_rows(args):
+    import mu_oracle
+    from paper_2012_03667_b200.mu_grid import MuParams, grid_for
+    p = MuParams()
+    g = grid_for(p)
+    shape = (g.n_s, g.n_4)
+    A, B, C = np.ones(shape, complex), np.full(shape, 0.3 + 0j), np.ones(shape, complex)
+    Aq, Bq, Cq = (mu_oracle.interp2d(g, X) for X in (A, B, C))
+    t0 = time.perf_counter()
+    for i in args:
+        mu_oracle.sweep_row(g, p, int(i), A, B, C, Aq, Bq, Cq)
+    return time.perf_counter() - t0
+
+
+def mu_cpu_rate(budget_s: float):
+    """The finite-mu CPU oracle (numpy, oracle/mu_oracle.py) on a row sample
+    of config 3, one process per host core.  There is no reference CPU path
+    for finite mu: this is the restatement, kind "port"."""
+    import multiprocessing as mp
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    cores = min(os.cpu_count() or 1, 32)
+    t1 = _mu_cpu_rows([8192])
+    per_core = max(1, int(budget_s / max(t1, 1e-3)))
+    rows = np.arange(cores * per_core) * 131 % (128 * 128)
+    chunks = [rows[c::cores].tolist() for c in range(cores)]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_mu_cpu_rows, chunks)
+    dt = time.perf_counter() - t0
+    pts = rows.size * 128 * 128 * 32
+    return pts / dt, {"rows": int(rows.size), "points": int(pts), "seconds": dt, "cores": cores}
+
+
+def mu_bench(p, torch, dev, flush, args, peak, no_cpu):
+    """BASELINE configs 3-4 (finite chemical potential; no reference path,
+    parity against oracle/mu_oracle.py).  Config 3: mu = 0.2 GeV on the
+    128 x 128 external / 128 x 128 x 32 internal grids (8.59e9 nominal
+    integrand points per iteration): one on-device iteration timed per step
+    with the state resident and L2 flushed, time to solution, and the public
+    API end to end.  Config 4: 32 independent solves with mu at the midpoints
+    of 32 equal cells of [0, 0.4] GeV on the same grids (replicas)."""
+    from paper_2012_03667_b200.finite_mu import MuSweeper, solve_mu, solve_mu_batch
+    from paper_2012_03667_b200.mu_grid import MuParams, grid_for
+    prm = MuParams()
+    g = grid_for(prm)
+    out = {"vertex": prm.vertex, "grids": "external 128 |p| x 128 p4, internal 128 |q| x 128 q4 x 32 cos(theta)"}
+    with MuSweeper(g, prm) as sw:
+        t0 = time.perf_counter()
+        sol = sw.solve(prm)  # warm-up; counts the evaluated points
+        wall_first = time.perf_counter() - t0
+        st = sw.stats()
+        A0 = torch.from_numpy(np.full(g.n_ext, 1.0 + 0j)).to(dev)
+        B0 = torch.from_numpy(np.full(g.n_ext, 0.3 + 0j)).to(dev)
+        C0 = torch.from_numpy(np.full(g.n_ext, 1.0 + 0j)).to(dev)
+        stream = torch.cuda.Stream(device=dev)
+        sp = stream.cuda_stream
+        steps = max(3, min(args.steps, 20))
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        with torch.cuda.stream(stream):
+            for w in range(args.warmup):
+                sw.load_device(A0.data_ptr(), B0.data_ptr(), C0.data_ptr(), sp)
+                sw.resume(1, sp)
+            for e0, e1 in ev:
+                sw.load_device(A0.data_ptr(), B0.data_ptr(), C0.data_ptr(), sp)
+                flush.fill_(1)
+                e0.record(stream)
+                sw.resume(1, sp)
+                e1.record(stream)
+            stream.synchronize()
+        ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+        t_it = float(np.median(ms)) / 1e3
+        # time to solution on the device (one cooperative launch)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        sol = sw.solve(prm)
+        e1.record()
+        torch.cuda.synchronize()
+        tts_wall = time.perf_counter() - t0
+        tts_dev = e0.elapsed_time(e1) / 1e3
+    # end to end through the public API: grid upload, H2D of the initial
+    # state, the loop, D2H of A, B, C and the history
+    t0 = time.perf_counter()
+    sol_e = solve_mu(prm, g)
+    e2e = time.perf_counter() - t0
+    achieved = st["evaluated_points"] * MU_FLOP_PER_POINT / t_it / 1e12
+    out["config3"] = {
+        "mu": prm.mu, "ms_per_iteration": 1e3 * t_it, "steps": steps, "l2": "flushed before every timed step",
+        "nominal_points_per_iteration": st["nominal_points"], "evaluated_points_per_iteration": st["evaluated_points"],
+        "nominal_points_per_s": st["nominal_points"] / t_it, "evaluated_points_per_s": st["evaluated_points"] / t_it,
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if peak else None, "flop_per_point": MU_FLOP_PER_POINT,
+                     "flop_source": "executed FP64 work per evaluated point from the ncu SASS mix (DFMA = 2)"},
+        "time_to_solution": {"iterations": sol.iterations, "converged": sol.converged, "seconds_device": tts_dev,
+                             "seconds_wall": tts_wall, "first_call_wall": wall_first,
+                             "points_per_s": st["nominal_points"] * sol.iterations / tts_dev},
+        "e2e": {"api": "paper_2012_03667_b200.finite_mu.solve_mu(MuParams(), grid)", "seconds": e2e,
+                "iterations": sol_e.iterations, "points_per_s": st["nominal_points"] * sol_e.iterations / e2e,
+                "h2d_bytes": 3 * 16 * g.n_ext, "d2h_bytes": 3 * 16 * g.n_ext + 32 * (sol_e.iterations + 1)},
+        "M_ir": str(sol.mass[0, g.n_4 // 2]),
+    }
+    mus = [0.4 * (k + 0.5) / 32 for k in range(32)]
+    t0 = time.perf_counter()
+    sols = solve_mu_batch(mus, prm, g)
+    t4 = time.perf_counter() - t0
+    out["config4"] = {"solves": len(mus), "mu_range": [mus[0], mus[-1]], "seconds": t4, "solves_per_s": len(mus) / t4,
+                      "seconds_per_solve": t4 / len(mus), "iterations": [s.iterations for s in sols],
+                      "converged": int(sum(s.converged for s in sols)),
+                      "nominal_points_per_s": st["nominal_points"] * sum(s.iterations for s in sols) / t4,
+                      "layout": "one sweeper, 32 on-device solves back to back on 1 GPU (replicas; 4 per GPU at 8)"}
+    if not no_cpu:
+        rate, info = mu_cpu_rate(float(os.environ.get("BENCH_MU_CPU_S", "8")))
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port",
+                               "sample": f"{info['rows']} config-3 rows x full 128x128x32 block, numpy oracle "
+                                         f"oracle/mu_oracle.py ({info['seconds']:.1f} s)"}
+    return out
+
+
 def run_ours_distributed(args):
     from paper_2012_03667_b200 import distributed as D
     return D.bench_main(args, METRIC, UNIT, CFG2, FLOP_PER_POINT)
@@ -475,6 +600,7 @@ def main():
     ap.add_argument("--no-tts", action="store_true")
     ap.add_argument("--no-interp", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-mu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
