@@ -459,6 +459,33 @@ def interp_bench(p, nat, torch, dev, hbm):
     t0 = time.perf_counter()
     p.interp_linear_batch(x, v, q, mode="direct")
     res["e2e_host_arrays_queries_per_s"] = n / (time.perf_counter() - t0)
+    # cubic half of config 1: natural cubic spline (no reference routine,
+    # SPEC.md:229; parity vs scipy + numpy restatement in tests/test_cubic.py)
+    from paper_2012_03667_b200.interpolation import interp_cubic_batch, natural_cubic_coefficients
+    dc = torch.from_numpy(natural_cubic_coefficients(x, v)).to(dev)
+    for mode_name, mode in (("cubic_search", nat.BATCH_SEARCH), ("cubic_direct", nat.BATCH_DIRECT)):
+        ts = []
+        for r in range(8):
+            flush.fill_(0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            err = nat.DseErr()
+            s = torch.cuda.current_stream().cuda_stream
+            e0.record()
+            rc = lib.dse_interp_cubic_batch_device(dx.data_ptr(), dv.data_ptr(), dc.data_ptr(), 512, dq.data_ptr(), n,
+                                                   mode, out.data_ptr(), idx.data_ptr(), s, ctypes.byref(err))
+            e1.record()
+            nat.raise_for(rc, err)
+            torch.cuda.synchronize()
+            if r >= 2:
+                ts.append(e0.elapsed_time(e1) / 1e3)
+        t = float(np.median(ts))
+        gbs = n * 20 / t / 1e9
+        res[mode_name] = {"queries_per_s": n / t, "seconds": t, "achieved_gbs": gbs,
+                          "frac_hbm": gbs / hbm[0], "peak_gbs": hbm[0], "peak_source": hbm[1],
+                          "bytes_per_query": 20}
+    t0 = time.perf_counter()
+    interp_cubic_batch(x, v, q, mode="direct")
+    res["cubic_e2e_host_arrays_queries_per_s"] = n / (time.perf_counter() - t0)
     return res
 
 

@@ -87,6 +87,12 @@ _PROTOS = [
                                                       ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                                       ctypes.POINTER(DseErr)]),
+    ("dse_interp_cubic_batch", ctypes.c_int, [f64p, f64p, f64p, ctypes.c_int64, f64p, ctypes.c_int64, ctypes.c_int,
+                                              f64p, i32p, ctypes.POINTER(DseErr)]),
+    ("dse_interp_cubic_batch_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                     ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                                     ctypes.POINTER(DseErr)]),
     ("dse_solve_load", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                       ctypes.POINTER(DseErr)]),
     ("dse_solve_resume", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
