@@ -73,6 +73,9 @@ struct MuArgs {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+#ifndef DSE_MU_MINB
+#define DSE_MU_MINB 2  // CTAs per SM the register budget is cut for (A/B: scripts/mu_ab.sh)
+#endif
 
 // clamped linear rule of the reference along one axis (interpolation.py:71-72, :125-132)
 __device__ __forceinline__ double axis_lin(bool in, double x0, double x1, double v0, double v1, double q) {
@@ -240,7 +243,7 @@ __device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, in
 __device__ __forceinline__ double hyp(double x, double y) { return hypot(x, y); }
 
 template <int V>
-__global__ void __launch_bounds__(kThreads, 1) mu_solve_kernel(MuArgs a) {
+__global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs a) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) double smem[];
     double* etbl = smem;                                           // 2^bits
