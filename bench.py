@@ -195,7 +195,7 @@ def run_ours(args):
     kernel_s = t_total / args.steps
     peak = ctypes_fp64_peak(nat, local)
     achieved = st["evaluated_points"] * FLOP_PER_POINT / kernel_s / 1e12
-    other = p.Arithmetic.EXACT if arith is p.Arithmetic.FAST else p.Arithmetic.FAST
+    other = p.Arithmetic.EXACT if arith is not p.Arithmetic.EXACT else p.Arithmetic.PAIRS
     sw_o = p.GpuSweeper(grid, params, p.InterpStrategy.PRECOMPUTED_INDEX, other, local)
     ms_o = time_device_steps(torch, sw_o, A, B, stream, flush, min(args.steps, 20), args.warmup)
     t_o = sum(ms_o) / 1e3 / len(ms_o)
@@ -208,7 +208,8 @@ def run_ours(args):
     a_pin = torch.ones(n, dtype=torch.float64).pin_memory()
     b_pin = torch.full((n,), 0.3, dtype=torch.float64).pin_memory()
     a_h, b_h = a_pin.numpy(), b_pin.numpy()
-    variant_name = "indexed-gpu-exact" if arith is p.Arithmetic.EXACT else "indexed-gpu"
+    variant_name = {p.Arithmetic.EXACT: "indexed-gpu-exact", p.Arithmetic.FAST: "indexed-gpu",
+                    p.Arithmetic.PAIRS: "indexed-gpu-pairs"}[arith]
     variant = p.VARIANTS[variant_name]
     for _ in range(2):
         p.iterate_once(grid, a_h, b_h, params_tiny, variant)
@@ -623,7 +624,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--arith", choices=["exact", "fast"], default=os.environ.get("DSE_BENCH_ARITH", "fast"))
+    ap.add_argument("--arith", choices=["exact", "fast", "pairs"], default=os.environ.get("DSE_BENCH_ARITH", "fast"))
     ap.add_argument("--no-tts", action="store_true")
     ap.add_argument("--no-interp", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -8,7 +8,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "dse_b200.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", "dse_device.cuh"), os.path.join(HERE, "csrc", "dse_mu.cu"), os.path.join(ROOT, "include", "dse_b200.h")]
+DEPS = SOURCES + [os.path.join(HERE, "csrc", "dse_device.cuh"), os.path.join(HERE, "csrc", "dse_mu.cu"), os.path.join(HERE, "csrc", "dse_pairs.cuh"), os.path.join(ROOT, "include", "dse_b200.h")]
 OUT = os.path.join(HERE, "libdse_b200.so")
 # bounds-checked diagnostic build (tests/test_gpu_checked.py): compute-sanitizer is closed on this pool
 OUT_CHECKED = os.path.join(ROOT, "build", "libdse_checked.so")

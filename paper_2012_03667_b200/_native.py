@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("DSE_LIB") or os.path.join(os.path.dirname(os.path.abs
 DSE_OK, DSE_EPARAM, DSE_ENUMERIC, DSE_EENV = 0, 1, 2, 3
 INTERP_SEARCH, INTERP_INDEXED = 0, 1
 BATCH_SEARCH, BATCH_DIRECT = 0, 1
-ARITH_EXACT, ARITH_FAST, ARITH_MOMENTS = 0, 1, 2
+ARITH_EXACT, ARITH_FAST, ARITH_MOMENTS, ARITH_PAIRS = 0, 1, 2, 3
 
 f64p = ctypes.POINTER(ctypes.c_double)
 i64p = ctypes.POINTER(ctypes.c_int64)

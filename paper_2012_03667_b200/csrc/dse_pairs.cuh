@@ -1,0 +1,197 @@
+// dse_pairs.cuh -- "pairs" arithmetic (DSE_ARITH_PAIRS): the fast sweep with
+// the angular sum of every (row, node) pair factored into five moments that
+// are accumulated point by point, then contracted once per pair.  Included
+// by dse_b200.cu after the moment kernel (it reuses SweepArgs, the node
+// prologue, make_fastj_direct, the history/stop protocol).
+//
+// Per (row i, node j) the fast summands are e w/kappa (U(r) + V(r)/kappa)
+// (A) and e w/kappa (W(r) + X(kq)/kappa) (B) with coefficients constant over
+// the angular nodes (make_fastj_direct), kq = q2 - r, kp = r - p2 and
+// kappa = p2 + q2 - 2r.  So with rho = 1/kappa
+//     S0 = sum ew rho, S1 = sum ew rho r, T0 = sum ew rho^2, T1 = sum ew rho^2 r,
+//     T2 = sum ew rho^2 r^2
+// the moment-arithmetic contraction (dse_moment_kernel) applies with
+// M0 = S0, M1 = S1, M2 = sum ew rho^2 kq kp = -T2 + psum T1 - p2 q2 T0,
+// M3 = T1, M4 = T0, M5 = q2 T0 - T1.  Every integrand point is evaluated every
+// iteration (one exp, one reciprocal, 23 FP64 instructions); a numpy model of
+// exactly this order agrees with the reference's golden sweeps to <= 7.8e-14
+// (hybrid), the fast-arithmetic tolerance is 1e-12.
+//
+// Work: item t = (owned row r, group g of 32 consecutive nodes), one WARP
+// per item (lane = node, the lane runs all K angles), items dealt by atomic
+// ticket in decreasing order of evaluated nodes (host table) so warps never
+// wait on each other inside an iteration and the tail is cheap items.  Nodes
+// outside the row's exact-zero window (the sweep kernel's rule)
+// are not evaluated unless a dressing value is non-finite (then NaN reaches
+// the sum as in the reference).  A group's partial is the lane xor tree; the
+// warp finishing a row's last group sums the G partials in order g = 0..G-1
+// and finalises the row.  Results are bitwise independent of the grid size,
+// the schedule and the row sharding.
+
+constexpr int kPairsThreads = 256;
+#ifndef DSE_PAIRS_MINB
+#define DSE_PAIRS_MINB 2  // 3 (80 regs) 0.359, 4 (64 regs) 0.367 ms: occupancy is not the limit
+#endif
+#ifndef DSE_PAIRS_UNROLL
+#define DSE_PAIRS_UNROLL 8  // measured at config 2: 2 -> 0.368, 4 -> 0.356, 8 -> 0.351 ms
+#endif
+constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
+
+__global__ void __launch_bounds__(kPairsThreads, DSE_PAIRS_MINB) dse_pairs_kernel(SweepArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    double* q2 = sm;
+    double* sq = q2 + a.M;
+    double* meas = sq + a.M;
+    double* aqs = meas + a.M;
+    double* bqs = aqs + a.M;
+    double* dens = bqs + a.M;
+    double2* zz = reinterpret_cast<double2*>(dens + a.M);
+    double* etbl = reinterpret_cast<double*>(zz + a.K);
+    __shared__ double red[2 * (kPairsThreads / 32)];
+    __shared__ int s_bad;
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int j = tid; j < a.M; j += blockDim.x) {
+        q2[j] = __ldg(a.q2 + j);
+        sq[j] = __ldg(a.sq + j);
+        meas[j] = __ldg(a.meas + j);
+    }
+    for (int k = tid; k < a.K; k += blockDim.x) zz[k] = make_double2(__ldg(a.z + k), __ldg(a.zw + k));
+    for (int i = tid; i < (1 << kExpTableBits); i += blockDim.x) etbl[i] = __ldg(a.exp_tbl + i);
+    __syncthreads();
+    const unsigned tbl = smem_addr(etbl);
+    const ExpK ek{a.exp_c1, a.nrw2};
+    if (a.it_begin == 0 && a.hist && blockIdx.x == 0 && tid == 0)
+        write_history(a, 0, __longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
+                      a.X, a.X + a.N);
+    const int G = a.pr_G;
+    const int n_items = a.n_mrows * G;
+    for (int it = a.it_begin; it < a.it_end; ++it) {
+        const int cur = it & 1, nxt = cur ^ 1;
+        const double* Ac = a.X + (size_t)(2 * cur) * a.N;
+        const double* Bc = Ac + a.N;
+        double* An = a.X + (size_t)(2 * nxt) * a.N;
+        double* Bn = An + a.N;
+        double* dr = a.drow + (size_t)(2 * cur) * a.N;
+        if (tid == 0) s_bad = 0;
+        __syncthreads();
+        int bad = 0;
+        for (int j = tid; j < a.M; j += blockDim.x) {  // a_q, b_q, den at the internal nodes (F9)
+            const double qq = q2[j];
+            const double aq = a.aq_in ? __ldg(a.aq_in + j) : interp_internal(a, Ac, j, qq);
+            const double bq = a.bq_in ? __ldg(a.bq_in + j) : interp_internal(a, Bc, j, qq);
+            aqs[j] = aq;
+            bqs[j] = bq;
+            const double den = add(mul(mul(qq, aq), aq), mul(bq, bq));
+            dens[j] = den;
+            bad |= !isfinite(aq) || !isfinite(bq) || !isfinite(den);
+        }
+        if (bad) atomicOr(&s_bad, 1);
+        __syncthreads();
+        const bool any_bad = s_bad != 0;
+        // ---- items: one warp each, by ticket
+        for (;;) {
+            int t = 0;
+            if (lane == 0) t = (int)atomicAdd(a.ctr + cur, 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= n_items) break;
+            t = __ldg(a.pr_items + t);  // longest first: the iteration's tail is empty groups
+            const int r = t / G, g = t - r * G;
+            const int i = a.mrow[r];
+            const double p2 = __ldg(a.p2 + i), rp2 = 1.0 / p2, sqp = sqrt(p2);
+            const double a_p = __ldcg(Ac + i), b_p = __ldcg(Bc + i);
+            const int2 win = __ldg(a.pr_win + r);
+            const int j = 32 * g + lane;
+            const bool all = any_bad || !isfinite(a_p) || !isfinite(b_p);
+            const bool active = j < a.M && (all || (j >= win.x && j < win.y));
+            double sa = 0.0, sb = 0.0;
+            if (active) {
+                const double qq = q2[j];
+                const double psum = p2 + qq;
+                const double sqj = sq[j];
+                double S0 = 0.0, S1 = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0;
+#pragma unroll kPairsUnroll
+                for (int k = 0; k < a.K; ++k) {
+                    const double2 zk = zz[k];
+                    // rz in the reference's rounding (kernels.py:189: sqrt(p2) * (sqrt(q2) z)):
+                    // kappa = psum - 2 rz cancels near p2 = q2, z = 1, so rz must round as there
+                    const double rr = sqp * (sqj * zk.x);
+                    const double kap = fma(-2.0, rr, psum);
+                    const double ew = zk.y * exp_neg_k2(kap, ek, tbl);
+                    const double rho = rcp_nr(kap);
+                    const double t0 = ew * rho;
+                    S0 += t0;
+                    S1 = fma(t0, rr, S1);
+                    const double t4 = t0 * rho;
+                    T0 += t4;
+                    const double t5 = t4 * rr;
+                    T1 += t5;
+                    T2 = fma(t5, rr, T2);
+                }
+                const double M2 = fma(psum, T1, -T2) - (p2 * qq) * T0;
+                const double M5 = fma(qq, T0, -T1);
+                const FastJ f = make_fastj_direct(p2, a_p, b_p, qq, sq[j], meas[j], aqs[j], bqs[j], dens[j], a.coeff,
+                                                  rp2);
+                sa = fma(f.uA0, S0, fma(f.uA1, S1, fma(f.c2A2, M2, f.vA * T1)));
+                sb = fma(f.wB0, S0, fma(f.wB1, S1, fma(f.xB0, T0, f.xB1 * M5)));
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                sa += __shfl_xor_sync(0xffffffffu, sa, o);
+                sb += __shfl_xor_sync(0xffffffffu, sb, o);
+            }
+            if (lane == 0) {
+                a.pr_part[(size_t)r * G + g] = make_double2(sa, sb);
+                __threadfence();
+                const unsigned done = atomicAdd(a.pr_cnt + r, 1u);
+                if (done == (unsigned)G - 1) {  // last group of the row: sum the partials in order
+                    __threadfence();
+                    const double2* pp = a.pr_part + (size_t)r * G;
+                    double ta = 0.0, tb = 0.0;
+                    for (int q = 0; q < G; ++q) {
+                        const double2 v = __ldcg(pp + q);
+                        ta += v.x;
+                        tb += v.y;
+                    }
+                    a.pr_cnt[r] = 0u;
+                    double an = add(a.z1, ta), bn = add(a.m0z1, tb);
+                    if (!(isfinite(an) && isfinite(bn))) atomicMin(a.err_row + cur, (unsigned long long)i);
+                    if (a.relax != 1.0) {
+                        an = add(mul(a.relax, an), mul(sub(1.0, a.relax), a_p));
+                        bn = add(mul(a.relax, bn), mul(sub(1.0, a.relax), b_p));
+                    }
+                    An[i] = an;
+                    Bn[i] = bn;
+                    dr[i] = fabs(sub(an, a_p));
+                    dr[a.N + i] = fabs(sub(bn, b_p));
+                }
+            }
+        }
+        if (blockIdx.x == 0 && tid == 0) {
+            a.err_row[nxt] = kNoRow;
+            a.ctr[nxt] = 0u;
+        }
+        grid.sync();
+        double da = 0.0, db = 0.0;  // the sweep kernel's stop rule (iteration.py:34-39)
+        for (int q = tid; q < a.n_mrows; q += blockDim.x) {
+            const int i = a.mrow[q];
+            da = nanmax(da, __ldcg(dr + i));
+            db = nanmax(db, __ldcg(dr + a.N + i));
+        }
+        block_max2(da, db, red);
+        const unsigned long long er = *(volatile unsigned long long*)(a.err_row + cur);
+        const bool failed = er != kNoRow;
+        const bool conv = !failed && (da < a.xi) && (db < a.xi);
+        if (blockIdx.x == 0 && tid == 0) {
+            if (!failed) {
+                if (a.hist) write_history(a, it + 1, da, db, An, Bn);
+                a.status[0] = it + 1;
+                a.status[1] = conv ? 1 : 0;
+                a.status[3] = nxt;
+            } else {
+                a.status[2] = it + 1;
+            }
+        }
+        if (failed || conv) break;
+    }
+}

@@ -72,16 +72,21 @@ class Arithmetic(enum.Enum):
            the grid and omega, then O(N*M) work per iteration
            (dse_moment_kernel).  A different summation order: parity with the
            reference to the fast tolerance, not bitwise.
+    PAIRS: fast arithmetic, every integrand point evaluated every iteration,
+           with the angular sum of each (row, node) pair accumulated as five
+           moments and contracted once per pair (dse_pairs_kernel).  Parity
+           gated like FAST.
     """
 
     EXACT = "exact"
     FAST = "fast"
     MOMENTS = "moments"
+    PAIRS = "pairs"
 
 
 def _arith_code(arith: Arithmetic) -> int:
     return {Arithmetic.EXACT: nat.ARITH_EXACT, Arithmetic.FAST: nat.ARITH_FAST,
-            Arithmetic.MOMENTS: nat.ARITH_MOMENTS}[arith]
+            Arithmetic.MOMENTS: nat.ARITH_MOMENTS, Arithmetic.PAIRS: nat.ARITH_PAIRS}[arith]
 
 
 @dataclass(frozen=True)
@@ -120,6 +125,9 @@ VARIANTS = {
     # O(N M K) moment build (for solves; parity gated like the fast variants)
     "search-gpu-moments": _SEARCH.with_arith(Arithmetic.MOMENTS),
     "indexed-gpu-moments": _INDEXED.with_arith(Arithmetic.MOMENTS),
+    # fast arithmetic in the pair-moment form (same points per iteration)
+    "search-gpu-pairs": _SEARCH.with_arith(Arithmetic.PAIRS),
+    "indexed-gpu-pairs": _INDEXED.with_arith(Arithmetic.PAIRS),
     # the reference's names (solver.py:69-74) -> the GPU variant with that
     # strategy, in the bit-faithful exact arithmetic
     "search-seq": _SEARCH.with_arith(Arithmetic.EXACT),

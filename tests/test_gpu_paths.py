@@ -73,3 +73,18 @@ def test_moments_warps_per_row_bitwise_equal(n, m, k):
     for wpr in ("1", "2", "4", "8", "3"):
         x = _sweep(g, prm, {"DSE_MOM_WPR": wpr}, p.Arithmetic.MOMENTS)
         assert np.array_equal(ref[0], x[0]) and np.array_equal(ref[1], x[1]), wpr
+
+
+@pytest.mark.parametrize("n,m,k", [(128, 128, 64), (300, 1000, 16), (1024, 1024, 256)])
+def test_pairs_grid_size_bitwise_equal(n, m, k):
+    """The pairs kernel deals (row, 32-node group) items to warps by ticket;
+    the grid size changes who computes a group, never the order of any sum."""
+    g = p.build_grid(n, m, k, 1e-6, 1e4)
+    prm = p.ModelParams(N=n, m_rad=m, m_ang=k, xi=1e-10)
+    ref = _sweep(g, prm, {}, p.Arithmetic.PAIRS)
+    for blocks in ("1", "7", "150"):
+        x = _sweep(g, prm, {"DSE_PAIRS_BLOCKS": blocks}, p.Arithmetic.PAIRS)
+        assert np.array_equal(ref[0], x[0]) and np.array_equal(ref[1], x[1]), blocks
+    fast = _sweep(g, prm, {}, p.Arithmetic.FAST)
+    assert np.max(np.abs(ref[0] - fast[0]) / np.abs(fast[0])) < 1e-12
+    assert np.max(np.abs(ref[1] - fast[1])) / np.max(np.abs(fast[1])) < 1e-12

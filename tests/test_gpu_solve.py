@@ -26,7 +26,8 @@ def _hist(sol):
     return np.array([[r.iteration, r.max_delta_a, r.max_delta_b, *r.probe_a, *r.probe_b] for r in sol.history])
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "search-gpu-exact", "indexed-gpu", "indexed-gpu-moments"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "search-gpu-exact", "indexed-gpu", "indexed-gpu-moments",
+                                   "indexed-gpu-pairs"])
 def test_solve_default_config(vname):
     z, sol = _run("solve_default.npz", "default", p.VARIANTS[vname])
     assert sol.iterations == int(z["iterations"]) and sol.converged == bool(z["converged"])
@@ -39,7 +40,7 @@ def test_solve_default_config(vname):
 
 
 @pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu", "indexed-gpu-moments",
-                                   "search-gpu-moments"])
+                                   "search-gpu-moments", "indexed-gpu-pairs", "search-gpu-pairs"])
 def test_solve_config0_exact_iteration_count(vname):
     """Config 0 (128/128/64, xi=1e-10, b0=0.3): the reference converges in 2923 sweeps."""
     z, sol = _run("solve_c0.npz", "c0", p.VARIANTS[vname])
@@ -49,7 +50,7 @@ def test_solve_config0_exact_iteration_count(vname):
     assert h.shape == z["history"].shape
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu", "indexed-gpu-moments"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu", "indexed-gpu-moments", "indexed-gpu-pairs"])
 def test_solve_config2_first_10_sweeps(vname):
     """Config 2 (1024/1024/256) does not converge in the reference:
     parity = first 10 sweeps + converged=False at the same cap."""
@@ -59,7 +60,7 @@ def test_solve_config2_first_10_sweeps(vname):
     np.testing.assert_allclose(_hist(sol)[1:, 1:3], z["history"][1:, 1:3], rtol=1e-6)
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu", "indexed-gpu-moments"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu", "indexed-gpu-moments", "indexed-gpu-pairs"])
 def test_solve_large_substitute_relaxation(vname):
     """N=M=K=256 at relaxation 0.5: the reference converges in 421 iterations."""
     z, sol = _run("solve_sub256.npz", "sub256", p.VARIANTS[vname])

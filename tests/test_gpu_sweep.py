@@ -16,9 +16,9 @@ from conftest import golden, golden_grid, hybrid_rel, params_ns
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"exact": 1e-13, "fast": 1e-12, "moments": 1e-12}
+TOL = {"exact": 1e-13, "fast": 1e-12, "moments": 1e-12, "pairs": 1e-12}
 VAR = {"exact": p.VARIANTS["indexed-gpu-exact"], "fast": p.VARIANTS["indexed-gpu"],
-       "moments": p.VARIANTS["indexed-gpu-moments"]}
+       "moments": p.VARIANTS["indexed-gpu-moments"], "pairs": p.VARIANTS["indexed-gpu-pairs"]}
 
 
 def _params(S, name):
@@ -26,7 +26,7 @@ def _params(S, name):
     return params_ns(D=D, omega=om, m0=m0, z1=z1, coeff=c)
 
 
-@pytest.mark.parametrize("arith", ["exact", "fast", "moments"])
+@pytest.mark.parametrize("arith", ["exact", "fast", "moments", "pairs"])
 def test_sweep_vs_reference_golden(arith):
     S = golden("sweeps.npz")
     for name in S["names"]:
@@ -37,7 +37,7 @@ def test_sweep_vs_reference_golden(arith):
         assert ea <= TOL[arith] and eb <= TOL[arith], (name, ea, eb)
 
 
-@pytest.mark.parametrize("arith", ["exact", "fast", "moments"])
+@pytest.mark.parametrize("arith", ["exact", "fast", "moments", "pairs"])
 @pytest.mark.parametrize("tag", ["c0", "ragged", "sub256", "c2"])
 def test_sweep_vs_oracle_random_states(arith, tag):
     g = golden_grid(tag)
@@ -63,7 +63,7 @@ def test_search_and_indexed_bitwise_equal_and_deterministic():
         assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
 
 
-@pytest.mark.parametrize("arith", [p.Arithmetic.FAST, p.Arithmetic.MOMENTS])
+@pytest.mark.parametrize("arith", [p.Arithmetic.FAST, p.Arithmetic.MOMENTS, p.Arithmetic.PAIRS])
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_row_sharded_sweepers_assemble_bitwise(world, arith):
     """Rows owned by rank r of W (r, r+W, ...) reproduce the full sweep bitwise:
@@ -82,7 +82,7 @@ def test_row_sharded_sweepers_assemble_bitwise(world, arith):
     assert np.array_equal(ao, full[0]) and np.array_equal(bo, full[1])
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu-moments"])
+@pytest.mark.parametrize("vname", ["indexed-gpu-exact", "indexed-gpu-moments", "indexed-gpu-pairs"])
 def test_free_theory_and_chiral_limit(vname):
     g = golden_grid("small")
     free = params_ns(D=0.0, m0=0.01)
@@ -94,7 +94,7 @@ def test_free_theory_and_chiral_limit(vname):
         assert np.all(b == 0.0)
 
 
-@pytest.mark.parametrize("arith", ["exact", "fast", "moments"])
+@pytest.mark.parametrize("arith", ["exact", "fast", "moments", "pairs"])
 def test_numerical_failure_location(arith):
     E = golden("errors.npz")
     g = golden_grid("small")
