@@ -624,7 +624,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--arith", choices=["exact", "fast", "pairs"], default=os.environ.get("DSE_BENCH_ARITH", "fast"))
+    ap.add_argument("--arith", choices=["exact", "fast", "pairs"], default=os.environ.get("DSE_BENCH_ARITH", "pairs"))
     ap.add_argument("--no-tts", action="store_true")
     ap.add_argument("--no-interp", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
