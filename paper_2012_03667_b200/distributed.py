@@ -215,7 +215,7 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
     os.environ["DSE_DEVICE"] = str(local)
     grid = build_grid(cfg["N"], cfg["M"], cfg["K"], cfg["p2_min"], cfg["p2_max"])
     params = ModelParams(N=cfg["N"], m_rad=cfg["M"], m_ang=cfg["K"], xi=1e-10)
-    variant = VARIANTS["indexed-gpu"].with_threads(world)
+    variant = VARIANTS["indexed-gpu-pairs"].with_threads(world)
     sw, dev, rank, world, sweep_rows, gather, probe_fn, torch = _device_loop(grid, params, variant)
     loop = ShardedLoop(grid.n_ext, rank, world, sweep_rows, gather, probe_fn(()), xp=torch)
     a = torch.ones(grid.n_ext, dtype=torch.float64, device=dev)
@@ -287,7 +287,7 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
             "e2e": {"value": nominal * args.steps / float(te.item()), "unit": unit,
                     "h2d_bytes_per_step": 2 * grid.n_ext * 8, "d2h_bytes_per_step": 2 * grid.n_ext * 8,
                     "api": "paper_2012_03667_b200.iterate_once(grid, A, B, params, "
-                           "VARIANTS['indexed-gpu'].with_threads(W)) under torchrun"},
+                           "VARIANTS['indexed-gpu-pairs'].with_threads(W)) under torchrun"},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": None,
                          "flop_per_point": flop_per_point, "points": "evaluated, per GPU",
