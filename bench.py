@@ -317,33 +317,42 @@ def peak_hbm():
 
 
 def time_to_solution(p, torch, dev, arith):
+    """Device time of the whole on-device solve (one cooperative launch) for
+    config 0 and the 256^3 substitute, in the bench arithmetic and, for
+    comparison, the fast one (the other per-point form)."""
     out = {}
     cases = {
-        "config0_128x128x64": (dict(N=128, m_rad=128, m_ang=64, xi=1e-10, max_iterations=20000), 1.0),
-        "substitute_256x256x256_relax0.5": (dict(N=256, m_rad=256, m_ang=256, xi=1e-10, max_iterations=2000,
-                                                 relaxation=0.5), 1.0),
+        "config0_128x128x64": dict(N=128, m_rad=128, m_ang=64, xi=1e-10, max_iterations=20000),
+        "substitute_256x256x256_relax0.5": dict(N=256, m_rad=256, m_ang=256, xi=1e-10, max_iterations=2000,
+                                                relaxation=0.5),
     }
-    for name, (kw, _) in cases.items():
+    ariths = [arith] + ([p.Arithmetic.FAST] if arith is not p.Arithmetic.FAST else [])
+    for name, kw in cases.items():
         prm = p.ModelParams(**kw)
         g = p.build_grid(prm.N, prm.m_rad, prm.m_ang, prm.p2_min, prm.p2_max)
-        sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, arith)
-        A = torch.ones(prm.N, dtype=torch.float64, device=dev)
-        B = torch.full((prm.N,), 0.3, dtype=torch.float64, device=dev)
-        sw.solve_device(A.data_ptr(), B.data_ptr(), prm.max_iterations)  # warm-up
-        A.fill_(1.0)
-        B.fill_(0.3)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        e0.record()
-        it, conv = sw.solve_device(A.data_ptr(), B.data_ptr(), prm.max_iterations)
-        e1.record()
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        pts = sw.stats()["nominal_points"] * it
-        out[name] = {"iterations": it, "converged": conv, "seconds_device": e0.elapsed_time(e1) / 1e3,
-                     "seconds_wall": wall, "points_per_s": pts / wall}
-        sw.close()
+        for ar in ariths:
+            sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, ar)
+            A = torch.ones(prm.N, dtype=torch.float64, device=dev)
+            B = torch.full((prm.N,), 0.3, dtype=torch.float64, device=dev)
+            sw.solve_device(A.data_ptr(), B.data_ptr(), prm.max_iterations)  # warm-up
+            A.fill_(1.0)
+            B.fill_(0.3)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record()
+            it, conv = sw.solve_device(A.data_ptr(), B.data_ptr(), prm.max_iterations)
+            e1.record()
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+            pts = sw.stats()["nominal_points"] * it
+            rec = {"iterations": it, "converged": conv, "seconds_device": e0.elapsed_time(e1) / 1e3,
+                   "seconds_wall": wall, "points_per_s": pts / wall, "arith": ar.value}
+            if ar is arith:
+                out[name] = rec
+            else:
+                out[name][ar.value] = rec
+            sw.close()
     return out
 
 

@@ -17,15 +17,19 @@
 // exactly this order agrees with the reference's golden sweeps to <= 7.8e-14
 // (hybrid), the fast-arithmetic tolerance is 1e-12.
 //
-// Work: item t = (owned row r, group g of 32 consecutive nodes), one WARP
-// per item (lane = node, the lane runs all K angles), items dealt by atomic
+// Work: item t = (owned row r, group g of 32 consecutive nodes, chunk c of
+// the angles), one WARP per item (lane = node, the lane runs the chunk's
+// angles; C = 1 chunk unless the problem has too few (row, group) items to
+// fill the GPU -- C depends on N, M, K only, so every GPU and every row
+// sharding uses the same partition; the contraction is linear in the
+// moments, so each chunk contracts its own), items dealt by atomic
 // ticket in decreasing order of evaluated nodes (host table) so warps never
 // wait on each other inside an iteration and the tail is cheap items.  Nodes
 // outside the row's exact-zero window (the sweep kernel's rule)
 // are not evaluated unless a dressing value is non-finite (then NaN reaches
 // the sum as in the reference).  A group's partial is the lane xor tree; the
 // warp finishing a row's last group sums the G partials in order g = 0..G-1
-// and finalises the row.  Results are bitwise independent of the grid size,
+// and finalises the row (partials in order (g, c)).  Results are bitwise independent of the grid size,
 // the schedule and the row sharding.
 
 constexpr int kPairsThreads = 256;
@@ -64,8 +68,9 @@ __global__ void __launch_bounds__(kPairsThreads, DSE_PAIRS_MINB) dse_pairs_kerne
     if (a.it_begin == 0 && a.hist && blockIdx.x == 0 && tid == 0)
         write_history(a, 0, __longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
                       a.X, a.X + a.N);
-    const int G = a.pr_G;
-    const int n_items = a.n_mrows * G;
+    const int C = a.pr_C, G = a.pr_G, GC = G * C;
+    const int kc = (a.K + C - 1) / C;  // angles per chunk
+    const int n_items = a.n_mrows * GC;
     for (int it = a.it_begin; it < a.it_end; ++it) {
         const int cur = it & 1, nxt = cur ^ 1;
         const double* Ac = a.X + (size_t)(2 * cur) * a.N;
@@ -96,7 +101,8 @@ __global__ void __launch_bounds__(kPairsThreads, DSE_PAIRS_MINB) dse_pairs_kerne
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t >= n_items) break;
             t = __ldg(a.pr_items + t);  // longest first: the iteration's tail is empty groups
-            const int r = t / G, g = t - r * G;
+            const int r = t / GC, gc = t - r * GC, g = gc / C, c = gc - g * C;
+            const int k0 = c * kc, k1 = min(a.K, k0 + kc);
             const int i = a.mrow[r];
             const double p2 = __ldg(a.p2 + i), rp2 = 1.0 / p2, sqp = sqrt(p2);
             const double a_p = __ldcg(Ac + i), b_p = __ldcg(Bc + i);
@@ -111,7 +117,7 @@ __global__ void __launch_bounds__(kPairsThreads, DSE_PAIRS_MINB) dse_pairs_kerne
                 const double sqj = sq[j];
                 double S0 = 0.0, S1 = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0;
 #pragma unroll kPairsUnroll
-                for (int k = 0; k < a.K; ++k) {
+                for (int k = k0; k < k1; ++k) {
                     const double2 zk = zz[k];
                     // rz in the reference's rounding (kernels.py:189: sqrt(p2) * (sqrt(q2) z)):
                     // kappa = psum - 2 rz cancels near p2 = q2, z = 1, so rz must round as there
@@ -141,14 +147,14 @@ __global__ void __launch_bounds__(kPairsThreads, DSE_PAIRS_MINB) dse_pairs_kerne
                 sb += __shfl_xor_sync(0xffffffffu, sb, o);
             }
             if (lane == 0) {
-                a.pr_part[(size_t)r * G + g] = make_double2(sa, sb);
+                a.pr_part[(size_t)r * GC + gc] = make_double2(sa, sb);
                 __threadfence();
                 const unsigned done = atomicAdd(a.pr_cnt + r, 1u);
-                if (done == (unsigned)G - 1) {  // last group of the row: sum the partials in order
+                if (done == (unsigned)GC - 1) {  // last item of the row: sum the partials in order
                     __threadfence();
-                    const double2* pp = a.pr_part + (size_t)r * G;
+                    const double2* pp = a.pr_part + (size_t)r * GC;
                     double ta = 0.0, tb = 0.0;
-                    for (int q = 0; q < G; ++q) {
+                    for (int q = 0; q < GC; ++q) {
                         const double2 v = __ldcg(pp + q);
                         ta += v.x;
                         tb += v.y;

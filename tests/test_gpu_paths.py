@@ -85,6 +85,9 @@ def test_pairs_grid_size_bitwise_equal(n, m, k):
     for blocks in ("1", "7", "150"):
         x = _sweep(g, prm, {"DSE_PAIRS_BLOCKS": blocks}, p.Arithmetic.PAIRS)
         assert np.array_equal(ref[0], x[0]) and np.array_equal(ref[1], x[1]), blocks
+    for chunks in ("2", "4"):  # angle chunks change the partition, not the result beyond rounding
+        x = _sweep(g, prm, {"DSE_PAIRS_CHUNKS": chunks}, p.Arithmetic.PAIRS)
+        assert np.max(np.abs(ref[0] - x[0]) / np.abs(ref[0])) < 1e-13
     fast = _sweep(g, prm, {}, p.Arithmetic.FAST)
     assert np.max(np.abs(ref[0] - fast[0]) / np.abs(fast[0])) < 1e-12
     assert np.max(np.abs(ref[1] - fast[1])) / np.max(np.abs(fast[1])) < 1e-12
