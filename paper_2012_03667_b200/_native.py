@@ -74,6 +74,13 @@ _PROTOS = [
                                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                                 ctypes.POINTER(DseErr)]),
     ("dse_sweeper_check", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DseErr)]),
+    ("dse_sharded_sweep_pack", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t,
+                                              ctypes.POINTER(DseErr)]),
+    ("dse_sharded_assemble", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                            ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t,
+                                            ctypes.POINTER(DseErr)]),
+    ("dse_sweeper_state", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p),
+                                         ctypes.POINTER(ctypes.c_void_p)]),
     ("dse_solve", ctypes.c_int, [ctypes.c_void_p, f64p, ctypes.c_int64, f64p, f64p, i64p,
                                  ctypes.POINTER(ctypes.c_int), f64p, ctypes.POINTER(DseErr)]),
     ("dse_solve_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,

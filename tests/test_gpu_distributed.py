@@ -54,3 +54,61 @@ def test_sharded_sweep_world1_bitwise(nccl_world1):
     x = iterate_once_sharded(g, a, b, params_ns(), p.VARIANTS["indexed-gpu"].with_threads(1))
     y = p.iterate_once(g, a, b, params_ns(), p.VARIANTS["indexed-gpu"])
     assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+
+
+
+def _device_to_host(ptr, n):
+    from cuda.bindings import runtime as cudart  # cuda-python: a raw device pointer -> host
+    out = np.empty(n)
+    err, = cudart.cudaMemcpy(out.ctypes.data, ptr, n * 8, cudart.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+    assert int(err) == 0, err
+    return out
+
+
+@pytest.mark.parametrize("world,relax", [(1, 1.0), (3, 1.0), (4, 0.5)])
+def test_fused_sharded_step_equals_sweep(world, relax):
+    """FusedShardedStep's device steps (sweep+pack | all-gather | assemble)
+    reproduce the single-GPU sweep + blend + deltas bitwise.  The W ranks run
+    one after another on one GPU (no kernel waits on another); the
+    all-gather is the stack of their send buffers."""
+    import ctypes
+
+    import torch
+
+    from paper_2012_03667_b200 import _native as nat
+    from paper_2012_03667_b200.distributed import FusedShardedStep
+    g = golden_grid("default")
+    prm = params_ns()
+    rng = np.random.default_rng(5)
+    a, b = rng.uniform(1, 2, g.n_ext), rng.uniform(0.1, 1, g.n_ext)
+    ref_a, ref_b = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, p.Arithmetic.PAIRS).sweep(a, b)
+    if relax != 1.0:
+        ref_a = relax * ref_a + (1.0 - relax) * a
+        ref_b = relax * ref_b + (1.0 - relax) * b
+    dev = torch.device("cuda", 0)
+    ta, tb = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    sws = [p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, p.Arithmetic.PAIRS, 0, rows=(r, world))
+           for r in range(world)]
+    steps = [FusedShardedStep(sw, g.n_ext, world, dev, None, relax) for sw in sws]
+    sp = torch.cuda.current_stream(dev).cuda_stream
+    lib = nat.load()
+    for st in steps:
+        st.load(ta, tb, sp)
+    for st in steps:  # every rank sweeps and packs its rows
+        err = nat.DseErr()
+        nat.raise_for(lib.dse_sharded_sweep_pack(st.sw.handle, st.send.data_ptr(), st.per, sp,
+                                                 ctypes.byref(err)), err)
+    recv = torch.stack([st.send for st in steps])
+    for st in steps:  # every rank assembles the same full state
+        err = nat.DseErr()
+        nat.raise_for(lib.dse_sharded_assemble(st.sw.handle, recv.data_ptr(), world, st.per, relax,
+                                               st.delta.data_ptr(), sp, ctypes.byref(err)), err)
+    torch.cuda.synchronize()
+    for st in steps:
+        out_a = _device_to_host(st.state_ptrs[0], g.n_ext)
+        out_b = _device_to_host(st.state_ptrs[1], g.n_ext)
+        assert np.array_equal(out_a, ref_a) and np.array_equal(out_b, ref_b)
+        d = st.delta.cpu().numpy()
+        assert d[0] == np.max(np.abs(ref_a - a)) and d[1] == np.max(np.abs(ref_b - b))
+    for sw in sws:
+        sw.close()
