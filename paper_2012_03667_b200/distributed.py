@@ -328,6 +328,32 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
     except Exception:  # noqa: BLE001
         peak = None
     achieved = float(evald.item()) * flop_per_point / t * args.steps / 1e12 / world  # per GPU
+    # BASELINE config 4 (finite-mu sweep, replicas): rank r solves the mu
+    # values r, r + W, ... of the 32 midpoints on [0, 0.4] GeV on its GPU;
+    # device-timed per rank (events around the rank's solves), max over ranks
+    mu_block = None
+    if os.environ.get("DSE_BENCH_MU", "1") != "0":
+        from .finite_mu import owned_mus, solve_mu_batch
+        from .mu_grid import MuParams, grid_for
+        mprm = MuParams()
+        mg = grid_for(mprm)
+        mus = [0.4 * (k + 0.5) / 32 for k in range(32)]
+        mine = owned_mus(mus, rank, world)
+        solve_mu_batch(mine[:1], mprm, mg, local)  # warm-up
+        torch.cuda.synchronize()
+        dist.barrier()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record()
+        sols = solve_mu_batch(mine, mprm, mg, local)
+        m1.record()
+        torch.cuda.synchronize()
+        tm = torch.tensor([m0.elapsed_time(m1) / 1e3], device=dev)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        its = torch.tensor([float(sum(s.iterations for s in sols))], device=dev)
+        dist.all_reduce(its, op=dist.ReduceOp.SUM)
+        mu_block = {"config4_solves": len(mus), "seconds": float(tm.item()), "solves_per_s": len(mus) / float(tm.item()),
+                    "solves_per_gpu": len(mine), "iterations_total": int(its.item()),
+                    "layout": "mu values dealt cyclically over the ranks, no collective (replicas)"}
     if rank == 0:
         print(json.dumps({
             "metric": metric, "value": nominal * args.steps / t, "unit": unit, "n_gpus": world,
@@ -349,6 +375,7 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
                          "peak_source": "measured: dse_fp64_peak DFMA probe (per GPU)"},
             "gpu_launches": launches,
             "clocks": clk.summary() if clk is not None else None,
+            "finite_mu": mu_block,
         }))
     sw.close()
     dist.destroy_process_group()

@@ -25,7 +25,7 @@ from . import _native as nat
 from .mu_grid import VERTICES, MuGrid, MuParams, build_mu_grid, grid_for
 
 __all__ = ["MuIterationRecord", "MuSolution", "MuSweeper", "solve_mu", "iterate_mu_once", "solve_mu_batch",
-           "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
+           "solve_mu_batch_sharded", "owned_mus", "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
 
 
 @dataclass(frozen=True)
@@ -204,6 +204,36 @@ def solve_mu_batch(mus, params: MuParams | None = None, grid: MuGrid | None = No
         for m in mus:
             out.append(sw.solve(replace(params, mu=float(m)), history=history))
     return out
+
+
+def owned_mus(mus, rank: int, world: int) -> list:
+    """The chemical potentials rank `rank` of `world` solves (config 4 is
+    replicas: mu values are dealt cyclically, no data-path collective)."""
+    return list(mus)[rank::world]
+
+
+def solve_mu_batch_sharded(mus, params: MuParams | None = None, grid: MuGrid | None = None, device: int = 0,
+                           rank: int | None = None, world: int | None = None) -> list:
+    """BASELINE config 4 across the ranks of a torch.distributed job (one
+    process per GPU): rank r solves owned_mus(mus, r, W) on its GPU, then the
+    (mu, iterations, converged, A, B, C) records are all-gathered so every
+    rank returns the full list in the order of `mus`."""
+    import torch.distributed as dist
+    if rank is None or world is None:
+        rank, world = dist.get_rank(), dist.get_world_size()
+    mine = owned_mus(mus, rank, world)
+    sols = solve_mu_batch(mine, params, grid, device)
+    recs = [(float(m), s.iterations, s.converged, s.A, s.B, s.C) for m, s in zip(mine, sols)]
+    if world == 1:
+        gathered = [recs]
+    else:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, recs)
+    by_mu = {}
+    for part in gathered:
+        for r in part:
+            by_mu[r[0]] = r
+    return [by_mu[float(m)] for m in mus]
 
 
 def interp_mu(grid: MuGrid, F, params: MuParams | None = None, device: int = 0) -> np.ndarray:

@@ -94,3 +94,51 @@ def test_owned_rows_partition():
     for world in (1, 2, 3, 8):
         allrows = np.sort(np.concatenate([owned_rows(1024, r, world) for r in range(world)]))
         assert np.array_equal(allrows, np.arange(1024))
+
+
+def test_owned_mus_partition():
+    from paper_2012_03667_b200.finite_mu import owned_mus
+    mus = [0.4 * (k + 0.5) / 32 for k in range(32)]
+    for world in (1, 2, 3, 8):
+        parts = [owned_mus(mus, r, world) for r in range(world)]
+        assert sorted(m for p_ in parts for m in p_) == sorted(mus)
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
+    assert len(owned_mus(mus, 0, 8)) == 4  # BASELINE config 4: 4 mu values per GPU at 8 GPUs
+
+
+def _run_mu(rank, world, port, q):
+    """solve_mu_batch_sharded's partition and all_gather_object over gloo,
+    with the GPU solve replaced by a test double (a deterministic fake)."""
+    import types
+
+    from paper_2012_03667_b200 import finite_mu
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def fake_batch(mus, params=None, grid=None, device=0, history=False):
+        return [types.SimpleNamespace(iterations=int(100 * m) + rank * 0, converged=True,
+                                      A=np.full(2, m), B=np.full(2, 2 * m), C=np.full(2, 3 * m)) for m in mus]
+
+    finite_mu.solve_mu_batch = fake_batch
+    mus = [0.4 * (k + 0.5) / 32 for k in range(32)]
+    recs = finite_mu.solve_mu_batch_sharded(mus, grid=object())
+    q.put((rank, [(r[0], r[1], float(r[3][0])) for r in recs]))
+    dist.destroy_process_group()
+
+
+def test_mu_batch_sharded_gathers_in_order():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run_mu, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    mus = [0.4 * (k + 0.5) / 32 for k in range(32)]
+    for r in range(world):
+        assert [x[0] for x in out[r]] == mus
+        assert all(x[2] == x[0] and x[1] == int(100 * x[0]) for x in out[r])
