@@ -250,10 +250,12 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
 
     from . import VARIANTS, ModelParams, build_grid, iterate_once
     from . import _native as nat
-    # NCCL prints its version banner on stdout at the first communicator
-    # unless told otherwise; the bench contract is ONE JSON line on stdout
-    if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
-        os.environ["NCCL_DEBUG"] = "WARN"
+    # the bench contract is ONE JSON line on stdout: the NCCL/c10d version
+    # banner (printed on fd 1 at the first communicator) goes to stderr
+    import sys
+    sys.stdout.flush()
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
     dist.init_process_group("nccl")
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -354,6 +356,9 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
         mu_block = {"config4_solves": len(mus), "seconds": float(tm.item()), "solves_per_s": len(mus) / float(tm.item()),
                     "solves_per_gpu": len(mine), "iterations_total": int(its.item()),
                     "layout": "mu values dealt cyclically over the ranks, no collective (replicas)"}
+    sys.stdout.flush()
+    os.dup2(saved_stdout, 1)
+    os.close(saved_stdout)
     if rank == 0:
         print(json.dumps({
             "metric": metric, "value": nominal * args.steps / t, "unit": unit, "n_gpus": world,
