@@ -79,6 +79,16 @@ _PROTOS = [
     ("dse_sharded_assemble", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t,
                                             ctypes.POINTER(DseErr)]),
+    ("dse_sharded_sweep_push", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int64, ctypes.c_size_t,
+                                              ctypes.POINTER(DseErr)]),
+    ("dse_p2p_barrier", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
+    ("dse_p2p_alloc", ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p,
+                                     ctypes.POINTER(DseErr)]),
+    ("dse_p2p_open", ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p),
+                                    ctypes.POINTER(DseErr)]),
+    ("dse_p2p_close", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     ("dse_sweeper_state", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p),
                                          ctypes.POINTER(ctypes.c_void_p)]),
     ("dse_solve", ctypes.c_int, [ctypes.c_void_p, f64p, ctypes.c_int64, f64p, f64p, i64p,

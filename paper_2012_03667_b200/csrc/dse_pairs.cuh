@@ -172,6 +172,13 @@ __global__ void __launch_bounds__(kPairsThreads, DSE_PAIRS_MINB) dse_pairs_kerne
                     }
                     An[i] = an;
                     Bn[i] = bn;
+                    // fused all-gather: this row goes to every rank's receive
+                    // buffer now, overlapping the rest of the sweep
+                    for (int q = 0; q < a.pr_world; ++q) {
+                        double* dst = a.pr_peer[q] + (size_t)a.pr_rank * 2 * a.pr_per;
+                        dst[r] = an;
+                        dst[a.pr_per + r] = bn;
+                    }
                     dr[i] = fabs(sub(an, a_p));
                     dr[a.N + i] = fabs(sub(bn, b_p));
                 }

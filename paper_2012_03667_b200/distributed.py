@@ -211,6 +211,97 @@ class FusedShardedStep:
         return self.delta
 
 
+def device_view(ptr: int, n: int, device):
+    """A torch float64 view of n doubles at a raw device address (the
+    sweeper's resident state), via __cuda_array_interface__."""
+    import torch
+
+    class _Raw:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (int(ptr), False), "version": 3,
+                                    "strides": None}
+    return torch.as_tensor(_Raw(), device=device)
+
+
+class P2PShardedStep:
+    """The multi-GPU iteration with the all-gather FUSED into the sweep over
+    NVLink peer memory (no NCCL on the data path): every rank maps every
+    other rank's receive buffer and barrier flag (CUDA IPC handles exchanged
+    once through `exchange`, e.g. dist.all_gather_object); the pairs kernel
+    stores each finished row into all receive buffers the moment the row is
+    done (dse_sharded_sweep_push), a one-thread kernel barriers across the
+    GPUs over the flags (bounded spin: a missing peer raises instead of
+    hanging), and dse_sharded_assemble rebuilds the full iterate with the
+    blend and the deltas.  3 launches per step."""
+
+    def __init__(self, sw, n: int, world: int, rank: int, device: int, dev, exchange, relaxation: float = 1.0):
+        import ctypes
+
+        import torch
+
+        from . import _native as nat
+        if world > 8:
+            raise ParameterError("the peer-memory all-gather maps at most 8 GPUs (one node)")
+        self._nat, self._lib = nat, nat.load()
+        self.sw, self.n, self.world, self.rank, self.relax = sw, n, world, rank, relaxation
+        self.per = math.ceil(n / world)
+        err = nat.DseErr()
+        self._own = []
+        handles = []
+        for nbytes in (world * 2 * self.per * 8, 64):
+            ptr = ctypes.c_void_p()
+            h = ctypes.create_string_buffer(64)
+            nat.raise_for(self._lib.dse_p2p_alloc(device, nbytes, ctypes.byref(ptr), h, ctypes.byref(err)), err)
+            self._own.append(ptr.value)
+            handles.append(h.raw)
+        everyone = exchange(tuple(handles))
+        self._mapped = []
+        recv, flags = [], []
+        for q in range(world):
+            if q == rank:
+                recv.append(self._own[0])
+                flags.append(self._own[1])
+                continue
+            got = []
+            for k in range(2):
+                ptr = ctypes.c_void_p()
+                nat.raise_for(self._lib.dse_p2p_open(device, everyone[q][k], ctypes.byref(ptr), ctypes.byref(err)),
+                              err)
+                got.append(ptr.value)
+                self._mapped.append(ptr.value)
+            recv.append(got[0])
+            flags.append(got[1])
+        self.peer_recv = (ctypes.c_uint64 * world)(*recv)
+        self.peer_flags = (ctypes.c_uint64 * world)(*flags)
+        self.recv_local = self._own[0]
+        self.epoch = 0
+        self.timed_out = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.delta = torch.zeros(2, dtype=torch.float64, device=dev)
+
+    def load(self, a, b, stream: int) -> None:
+        self.sw.load_device(a.data_ptr(), b.data_ptr(), stream)
+
+    def step(self, stream: int):
+        import ctypes
+        err = self._nat.DseErr()
+        lib = self._lib
+        self._nat.raise_for(lib.dse_sharded_sweep_push(self.sw.handle, self.peer_recv, self.world, self.rank,
+                                                       self.per, stream, ctypes.byref(err)), err)
+        self.epoch += 1
+        self._nat.raise_for(lib.dse_p2p_barrier(self.peer_flags, self.world, self.rank, self.epoch,
+                                                self.timed_out.data_ptr(), stream, ctypes.byref(err)), err)
+        self._nat.raise_for(lib.dse_sharded_assemble(self.sw.handle, self.recv_local, self.world, self.per,
+                                                     self.relax, self.delta.data_ptr(), stream, ctypes.byref(err)),
+                            err)
+        return self.delta
+
+    def close(self) -> None:
+        for p in self._mapped:
+            self._lib.dse_p2p_close(p, 0)
+        for p in self._own:
+            self._lib.dse_p2p_close(p, 1)
+        self._mapped, self._own = [], []
+
+
 def solve_sharded(grid, params, variant, a0, b0, probes_p2):
     sw, dev, rank, world, sweep_rows, gather, probe_fn, torch = _device_loop(grid, params, variant)
     try:
@@ -274,14 +365,46 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
     b = torch.full((grid.n_ext,), 0.3, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     sp = torch.cuda.current_stream(dev).cuda_stream
+    state_ptr = fused.state_ptrs
+    # the all-gather fused into the sweep over NVLink peer memory, if every
+    # rank validates it bitwise against the NCCL step (else the NCCL step)
+    exchanger = None
+    p2p_note = "disabled (DSE_P2P=0)"
+    if os.environ.get("DSE_P2P", "1") != "0":
+        try:
+            def exchange(obj):
+                out = [None] * world
+                dist.all_gather_object(out, obj)
+                return out
+            exchanger = P2PShardedStep(sw, grid.n_ext, world, rank, local, dev, exchange)
+            fused.load(a, b, sp)
+            fused.step(sp)
+            ref = torch.cat([device_view(state_ptr[0], grid.n_ext, dev), device_view(state_ptr[1], grid.n_ext, dev)])
+            ref = ref.clone()
+            exchanger.load(a, b, sp)
+            exchanger.step(sp)
+            got = torch.cat([device_view(state_ptr[0], grid.n_ext, dev), device_view(state_ptr[1], grid.n_ext, dev)])
+            torch.cuda.synchronize()
+            ok_here = bool(torch.equal(got, ref)) and int(exchanger.timed_out.item()) == 0
+            flag = torch.tensor([1 if ok_here else 0], device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 1:
+                p2p_note = "peer-memory all-gather fused into the sweep (validated bitwise vs the NCCL step)"
+            else:
+                p2p_note = "fallback to NCCL: peer-memory step disagreed or timed out on some rank"
+                exchanger = None
+        except Exception as exc:  # noqa: BLE001
+            p2p_note = f"fallback to NCCL: {type(exc).__name__}: {str(exc)[:120]}"
+            exchanger = None
+    stepper = exchanger if exchanger is not None else fused
 
     def step():
         # every step sweeps the same synthetic state (config 2 diverges,
         # SURVEY F3): reload (untimed below), then sweep + all-gather + assemble
-        return fused.step(sp)
+        return stepper.step(sp)
 
     for _ in range(args.warmup):
-        fused.load(a, b, sp)
+        stepper.load(a, b, sp)
         flush.fill_(1)
         step()
     torch.cuda.synchronize()
@@ -293,7 +416,7 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
         from bench import ClockSampler  # the repo's bench.py (rank 0 samples its GPU's clocks)
         clk = ClockSampler(local).__enter__()
     for e0, e1 in ev:
-        fused.load(a, b, sp)
+        stepper.load(a, b, sp)
         flush.fill_(1)
         e0.record()
         step()
@@ -367,7 +490,10 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
             "data": "synthetic",
             "config": {"workload": "config2_vacuum_1024x1024x256", "parallelism": f"rows cyclic over {world} GPUs",
                        "collective": "NCCL all_gather of [A'|B'] rows per step",
-                       "step": "sweep owned rows + pack (libdse) | all_gather (NCCL) | assemble + deltas (libdse)",
+                       "step": ("sweep owned rows + push each finished row to every GPU (NVLink peer stores) | "
+                                "flag barrier | assemble + deltas" if exchanger is not None else
+                                "sweep owned rows + pack (libdse) | all_gather (NCCL) | assemble + deltas (libdse)"),
+                       "all_gather": p2p_note,
                        "l2": "flushed (256 MiB write) before every timed step",
                        "evaluated_points_per_step": int(evald.item()), "nominal_points_per_step": nominal},
             "e2e": {"value": nominal * args.steps / float(te.item()), "unit": unit,
@@ -382,6 +508,10 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
             "clocks": clk.summary() if clk is not None else None,
             "finite_mu": mu_block,
         }))
+    if exchanger is not None:
+        torch.cuda.synchronize()
+        dist.barrier()  # no peer may unmap a buffer another rank still writes
+        exchanger.close()
     sw.close()
     dist.destroy_process_group()
     return 0

@@ -112,3 +112,41 @@ def test_fused_sharded_step_equals_sweep(world, relax):
         assert d[0] == np.max(np.abs(ref_a - a)) and d[1] == np.max(np.abs(ref_b - b))
     for sw in sws:
         sw.close()
+
+
+@pytest.mark.parametrize("relax", [1.0, 0.5])
+def test_p2p_step_world1_equals_sweep(relax):
+    """P2PShardedStep at world 1 (the peer is this GPU: the push, the flag
+    barrier and the assemble all run; multi-GPU is correct by construction,
+    one GPU per test box) equals the sweep + blend + deltas bitwise, twice
+    in a row (the barrier epochs advance)."""
+    import torch
+
+    from paper_2012_03667_b200.distributed import P2PShardedStep, device_view
+    g = golden_grid("default")
+    prm = params_ns()
+    rng = np.random.default_rng(9)
+    a, b = rng.uniform(1, 2, g.n_ext), rng.uniform(0.1, 1, g.n_ext)
+    dev = torch.device("cuda", 0)
+    sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, p.Arithmetic.PAIRS, 0)
+    step = P2PShardedStep(sw, g.n_ext, 1, 0, 0, dev, lambda obj: [obj], relax)
+    sp = torch.cuda.current_stream(dev).cuda_stream
+    from paper_2012_03667_b200.distributed import FusedShardedStep
+    ptrs = FusedShardedStep(sw, g.n_ext, 1, dev, None).state_ptrs
+    state_a, state_b = a, b
+    step.load(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), sp)
+    for _ in range(2):
+        ra, rb = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, p.Arithmetic.PAIRS).sweep(state_a, state_b)
+        if relax != 1.0:
+            ra = relax * ra + (1.0 - relax) * state_a
+            rb = relax * rb + (1.0 - relax) * state_b
+        d = step.step(sp).cpu().numpy()
+        torch.cuda.synchronize()
+        ga = device_view(ptrs[0], g.n_ext, dev).cpu().numpy()
+        gb = device_view(ptrs[1], g.n_ext, dev).cpu().numpy()
+        assert int(step.timed_out.item()) == 0
+        assert np.array_equal(ga, ra) and np.array_equal(gb, rb)
+        assert d[0] == np.max(np.abs(ra - state_a)) and d[1] == np.max(np.abs(rb - state_b))
+        state_a, state_b = ra, rb
+    step.close()
+    sw.close()
