@@ -247,7 +247,12 @@ class P2PShardedStep:
         err = nat.DseErr()
         self._own = []
         handles = []
-        for nbytes in (world * 2 * self.per * 8, 64):
+        # receive buffers double-buffered by step parity: a fast rank's push of
+        # step e+1 must not overwrite what a slow rank still assembles of step e
+        # (the push of e+2 waits for everyone's push of e+1, which follows
+        # their assemble of e in stream order)
+        self._slot = world * 2 * self.per
+        for nbytes in (2 * self._slot * 8, 64):
             ptr = ctypes.c_void_p()
             h = ctypes.create_string_buffer(64)
             nat.raise_for(self._lib.dse_p2p_alloc(device, nbytes, ctypes.byref(ptr), h, ctypes.byref(err)), err)
@@ -270,9 +275,9 @@ class P2PShardedStep:
                 self._mapped.append(ptr.value)
             recv.append(got[0])
             flags.append(got[1])
-        self.peer_recv = (ctypes.c_uint64 * world)(*recv)
+        self.peer_recv = [(ctypes.c_uint64 * world)(*[r + 8 * self._slot * par for r in recv]) for par in (0, 1)]
         self.peer_flags = (ctypes.c_uint64 * world)(*flags)
-        self.recv_local = self._own[0]
+        self.recv_local = [self._own[0] + 8 * self._slot * par for par in (0, 1)]
         self.epoch = 0
         self.timed_out = torch.zeros(1, dtype=torch.int32, device=dev)
         self.delta = torch.zeros(2, dtype=torch.float64, device=dev)
@@ -284,12 +289,13 @@ class P2PShardedStep:
         import ctypes
         err = self._nat.DseErr()
         lib = self._lib
-        self._nat.raise_for(lib.dse_sharded_sweep_push(self.sw.handle, self.peer_recv, self.world, self.rank,
+        par = self.epoch & 1
+        self._nat.raise_for(lib.dse_sharded_sweep_push(self.sw.handle, self.peer_recv[par], self.world, self.rank,
                                                        self.per, stream, ctypes.byref(err)), err)
         self.epoch += 1
         self._nat.raise_for(lib.dse_p2p_barrier(self.peer_flags, self.world, self.rank, self.epoch,
                                                 self.timed_out.data_ptr(), stream, ctypes.byref(err)), err)
-        self._nat.raise_for(lib.dse_sharded_assemble(self.sw.handle, self.recv_local, self.world, self.per,
+        self._nat.raise_for(lib.dse_sharded_assemble(self.sw.handle, self.recv_local[par], self.world, self.per,
                                                      self.relax, self.delta.data_ptr(), stream, ctypes.byref(err)),
                             err)
         return self.delta
