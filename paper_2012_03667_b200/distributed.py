@@ -119,7 +119,30 @@ def _torch_env():
     return torch, dist
 
 
+_LOOP_CACHE: dict = {}
+
+
 def _device_loop(grid, params, variant):
+    """ShardedLoop wiring (sweeper, rows, buffers, gather, probes), cached per
+    (grid, params, variant, rank, world) like the single-GPU sweeper cache
+    (solver._make_sweeper): repeated iterate_once / solve calls under
+    torchrun reuse the uploaded grid and plan."""
+    from .solver import _params_key
+    torch, dist = _torch_env()
+    key = (id(grid), _params_key(params), variant.interp, variant.arith, dist.get_rank(), dist.get_world_size(),
+           int(os.environ.get("LOCAL_RANK", torch.cuda.current_device())))
+    hit = _LOOP_CACHE.get(key)
+    if hit is not None and hit[0].grid is grid:
+        return hit
+    ctx = _device_loop_new(grid, params, variant)
+    for old in list(_LOOP_CACHE.values()):
+        old[0].close()
+    _LOOP_CACHE.clear()
+    _LOOP_CACHE[key] = ctx
+    return ctx
+
+
+def _device_loop_new(grid, params, variant):
     """ShardedLoop wired to libdse_b200 (sweep) + NCCL all-gather + device probes."""
     import ctypes
 
@@ -317,7 +340,7 @@ def solve_sharded(grid, params, variant, a0, b0, probes_p2):
         a, b, n, conv, hist = loop.run(a, b, params.xi, int(params.max_iterations), params.relaxation)
         return a.cpu().numpy(), b.cpu().numpy(), n, conv, hist
     finally:
-        sw.close()
+        pass  # the sweeper stays cached (_LOOP_CACHE)
 
 
 def iterate_once_sharded(grid, a, b, params, variant):
@@ -329,7 +352,7 @@ def iterate_once_sharded(grid, a, b, params, variant):
         an, bn = loop.sweep(at, bt)
         return an.cpu().numpy(), bn.cpu().numpy()
     finally:
-        sw.close()
+        pass  # the sweeper stays cached (_LOOP_CACHE)
 
 
 def bench_main(args, metric, unit, cfg, flop_per_point):
@@ -518,6 +541,8 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
         torch.cuda.synchronize()
         dist.barrier()  # no peer may unmap a buffer another rank still writes
         exchanger.close()
-    sw.close()
+    for ctx in list(_LOOP_CACHE.values()):
+        ctx[0].close()
+    _LOOP_CACHE.clear()
     dist.destroy_process_group()
     return 0
