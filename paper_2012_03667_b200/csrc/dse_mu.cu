@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
     for (int k = tid; k < a.m_4; k += kThreads) q4s[k] = __ldg(a.q4 + k);
     __syncthreads();
     const unsigned tbl = dse::smem_addr(etbl);
-    const int n_ext = a.n_s * a.n_4, m_int = a.m_s * a.m_4;
+    const int n_ext = a.n_s * a.n_4;
     long long it_done = a.it_begin;
     bool converged = false;
     for (int it = a.it_begin; it < a.it_end; ++it) {

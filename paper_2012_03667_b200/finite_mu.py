@@ -242,9 +242,3 @@ def interp_mu(grid: MuGrid, F, params: MuParams | None = None, device: int = 0) 
     with MuSweeper(grid, params, device) as sw:
         return sw.interp(F)
 
-
-def default_grid(params: MuParams | None = None) -> MuGrid:
-    return grid_for(MuParams() if params is None else params)
-
-
-_ = build_mu_grid  # re-exported
