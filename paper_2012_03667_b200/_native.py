@@ -140,6 +140,13 @@ _PROTOS = [
                                          ctypes.c_size_t, ctypes.POINTER(DseErr)]),
     ("dse_mu_solve_resume", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
     ("dse_mu_interp", ctypes.c_int, [ctypes.c_void_p, f64p, f64p, ctypes.POINTER(DseErr)]),
+    ("dse_mu_sharded_sweep_pack", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DseMuParams), ctypes.c_void_p,
+                                                 ctypes.c_int64, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
+    ("dse_mu_sharded_assemble", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                               ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t,
+                                               ctypes.POINTER(DseErr)]),
+    ("dse_mu_sharded_failure", ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
+    ("dse_mu_sweeper_state", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     ("dse_mu_sweeper_stats", ctypes.c_int, [ctypes.c_void_p, i64p, i64p, i32p, i64p]),
     ("dse_launch_count", ctypes.c_int64, []),
 ]

@@ -242,6 +242,54 @@ __device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, in
 
 __device__ __forceinline__ double hyp(double x, double y) { return hypot(x, y); }
 
+// relax * new + (1 - relax) * old per component, each operation rounded once
+__device__ __forceinline__ double2 mu_blend(double relax, double2 n, double2 o) {
+    const double om = __dsub_rn(1.0, relax);
+    return make_double2(__dadd_rn(__dmul_rn(relax, n.x), __dmul_rn(om, o.x)),
+                        __dadd_rn(__dmul_rn(relax, n.y), __dmul_rn(om, o.y)));
+}
+
+// Multi-GPU (finite_mu.solve_mu_sharded): pack the owned rows of the new
+// state into send[3][per] (complex), and rebuild the full state from the
+// gathered recv[world][3][per] with the blend and the per-function max
+// |new - old| (one CTA; max is exact, so order-free).
+__global__ void mu_pack_kernel(const double2* __restrict__ Xn, int n_ext, int r0, int w, int per,
+                               double2* __restrict__ send) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < per; k += gridDim.x * blockDim.x) {
+        const int i = r0 + k * w;
+        for (int f = 0; f < 3; ++f) send[f * per + k] = i < n_ext ? Xn[(size_t)f * n_ext + i] : make_double2(0.0, 0.0);
+    }
+}
+
+__global__ void __launch_bounds__(1024) mu_assemble_kernel(const double2* __restrict__ recv, int world, int per,
+                                                           int n_ext, double relax, double2* __restrict__ X,
+                                                           double* __restrict__ delta) {
+    __shared__ double red[3][32];
+    double d[3] = {0.0, 0.0, 0.0};
+    for (int i = threadIdx.x; i < n_ext; i += blockDim.x) {
+        const int r = i % world, k = i / world;
+        for (int f = 0; f < 3; ++f) {
+            double2 nv = recv[((size_t)r * 3 + f) * per + k];
+            const double2 ov = X[(size_t)f * n_ext + i];
+            if (relax != 1.0) nv = mu_blend(relax, nv, ov);
+            d[f] = fmax(d[f], hyp(nv.x - ov.x, nv.y - ov.y));
+            X[(size_t)f * n_ext + i] = nv;
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int f = 0; f < 3; ++f) {
+        double v = d[f];
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) red[f][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double v = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[threadIdx.x][w]);
+        delta[threadIdx.x] = v;
+    }
+}
+
 template <int V>
 __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs a) {
     cg::grid_group grid = cg::this_grid();
@@ -378,11 +426,10 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
                 double2 Bn = make_double2(a.m0z1 + s[2], s[3]);
                 const cplx cn = C(s[4], s[5]) * rcp(rc.p4t);
                 double2 Cn = make_double2(a.z1 + cn.x, cn.y);
-                if (a.relax != 1.0) {
-                    const double om = 1.0 - a.relax;
-                    An = make_double2(a.relax * An.x + om * va.x, a.relax * An.y + om * va.y);
-                    Bn = make_double2(a.relax * Bn.x + om * vb.x, a.relax * Bn.y + om * vb.y);
-                    Cn = make_double2(a.relax * Cn.x + om * vc.x, a.relax * Cn.y + om * vc.y);
+                if (a.relax != 1.0) {  // solver.py:249-251, one rounding per op (as mu_blend)
+                    An = mu_blend(a.relax, An, va);
+                    Bn = mu_blend(a.relax, Bn, vb);
+                    Cn = mu_blend(a.relax, Cn, vc);
                 }
                 const bool fin = isfinite(An.x) && isfinite(An.y) && isfinite(Bn.x) && isfinite(Bn.y) &&
                                  isfinite(Cn.x) && isfinite(Cn.y);
@@ -801,7 +848,7 @@ int dse_mu_solve_load(dse_mu_sweeper* s, const double* dA, const double* dB, con
     ok(err);
     if (!s || !dA || !dB || !dC) return fail(err, DSE_EPARAM, "null argument");
     CUDA_TRY(cudaSetDevice(s->device));
-    cudaStream_t st = stream ? (cudaStream_t)stream : s->stream;
+    cudaStream_t st = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     const size_t ne = (size_t)s->n_s * s->n_4;
     const double* src[3] = {dA, dB, dC};
     for (int f = 0; f < 3; ++f)
@@ -810,7 +857,6 @@ int dse_mu_solve_load(dse_mu_sweeper* s, const double* dA, const double* dB, con
     CUDA_TRY(cudaGetLastError());
     g_launches.fetch_add(1);
     s->it_next = 0;
-    if (stream) CUDA_TRY(cudaStreamSynchronize(st));
     return DSE_OK;
 }
 
@@ -819,7 +865,7 @@ int dse_mu_solve_resume(dse_mu_sweeper* s, int64_t n_iterations, uintptr_t strea
     if (!s || n_iterations < 1) return fail(err, DSE_EPARAM, "bad argument");
     CUDA_TRY(cudaSetDevice(s->device));
     cudaStream_t keep = s->stream;
-    if (stream) s->stream = (cudaStream_t)stream;
+    s->stream = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     mu::MuArgs a = mu_make_args(s, s->prm, (int)s->it_next, (int)(s->it_next + n_iterations), false, true, false);
     int rc = mu_launch(s, a, false, err);
     s->stream = keep;
@@ -848,6 +894,62 @@ int dse_mu_interp(dse_mu_sweeper* s, const double* F, double* out, dse_err* err)
         out[2 * j + 1] = nb[4 * j].y;
     }
     (void)ne;
+    return DSE_OK;
+}
+
+int dse_mu_sharded_sweep_pack(dse_mu_sweeper* s, const dse_mu_params* params, double* d_send, int64_t per,
+                              uintptr_t stream, dse_err* err) {
+    ok(err);
+    if (!s || !d_send || per < s->n_rows) return fail(err, DSE_EPARAM, "bad argument");
+    dse_mu_params p = params ? *params : s->prm;
+    int rc = mu_check_params(&p, err);
+    if (rc) return rc;
+    p.relaxation = 1.0;  // the blend is applied at assembly
+    CUDA_TRY(cudaSetDevice(s->device));
+    cudaStream_t keep = s->stream;
+    s->stream = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
+    mu::MuArgs a = mu_make_args(s, p, 0, 1, false, true, false);
+    rc = mu_launch(s, a, true, err);
+    if (!rc) {
+        const size_t ne = (size_t)s->n_s * s->n_4;
+        mu::mu_pack_kernel<<<(int)std::max<int64_t>(1, (per + 255) / 256), 256, 0, s->stream>>>(
+            s->d_X + 3 * ne, (int)ne, s->row_start, s->row_stride, (int)per, (double2*)d_send);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fail(err, DSE_EENV, "mu_pack_kernel: %s", cudaGetErrorString(e));
+        g_launches.fetch_add(1);
+    }
+    s->stream = keep;
+    return rc;
+}
+
+int dse_mu_sharded_assemble(dse_mu_sweeper* s, const double* d_recv, int64_t world, int64_t per, double relax,
+                            double* d_delta, uintptr_t stream, dse_err* err) {
+    ok(err);
+    const int64_t ne = s ? (int64_t)s->n_s * s->n_4 : 0;
+    if (!s || !d_recv || !d_delta || world < 1 || per * world < ne) return fail(err, DSE_EPARAM, "bad argument");
+    if (!(relax > 0.0 && relax <= 1.0)) return fail(err, DSE_EPARAM, "relaxation out of range");
+    CUDA_TRY(cudaSetDevice(s->device));
+    mu::mu_assemble_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
+        (const double2*)d_recv, (int)world, (int)per, (int)ne, relax, s->d_X, d_delta);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    return DSE_OK;
+}
+
+int dse_mu_sharded_failure(dse_mu_sweeper* s, uintptr_t stream, dse_err* err) {
+    // after a sharded sweep on `stream`: report a numerical failure of this rank's rows
+    ok(err);
+    if (!s) return fail(err, DSE_EPARAM, "null argument");
+    long long st[4];
+    CUDA_TRY(cudaMemcpyAsync(st, s->d_status, sizeof(st), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    if (st[2] == 0) return DSE_OK;
+    return mu_failure(s, s->prm, st[2], st[3], err);
+}
+
+int dse_mu_sweeper_state(dse_mu_sweeper* s, double** dX) {
+    if (!s || !dX) return DSE_EPARAM;
+    *dX = (double*)s->d_X;  // [3][n_ext] complex: A, B, C
     return DSE_OK;
 }
 

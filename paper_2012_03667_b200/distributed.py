@@ -508,6 +508,43 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
         mu_block = {"config4_solves": len(mus), "seconds": float(tm.item()), "solves_per_s": len(mus) / float(tm.item()),
                     "solves_per_gpu": len(mine), "iterations_total": int(its.item()),
                     "layout": "mu values dealt cyclically over the ranks, no collective (replicas)"}
+        # config 3 with its 16384 external points sharded over the ranks: one
+        # iteration = sweep the owned points + pack | NCCL all-gather | assemble
+        import ctypes
+        from .finite_mu import MuSweeper, _c_params
+        per_mu = math.ceil(mg.n_ext / world)
+        send = torch.zeros((3, per_mu, 2), dtype=torch.float64, device=dev)
+        recv = torch.zeros((world, 3, per_mu, 2), dtype=torch.float64, device=dev)
+        dl = torch.zeros(3, dtype=torch.float64, device=dev)
+        init = [torch.full((mg.n_ext,), v, dtype=torch.complex128, device=dev) for v in (1.0, 0.3, 1.0)]
+        cpm = _c_params(mprm)
+        lib = nat.load()
+        err = nat.DseErr()
+        ms = []
+        with MuSweeper(mg, mprm, local, row_start=rank, row_stride=world) as msw:
+            for k in range(args.warmup + 5):
+                nat.raise_for(lib.dse_mu_solve_load(msw.handle, *[t.data_ptr() for t in init], sp,
+                                                    ctypes.byref(err)), err)
+                flush.fill_(1)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                nat.raise_for(lib.dse_mu_sharded_sweep_pack(msw.handle, ctypes.byref(cpm), send.data_ptr(), per_mu,
+                                                            sp, ctypes.byref(err)), err)
+                dist.all_gather_into_tensor(recv, send)
+                nat.raise_for(lib.dse_mu_sharded_assemble(msw.handle, recv.data_ptr(), world, per_mu, 1.0,
+                                                          dl.data_ptr(), sp, ctypes.byref(err)), err)
+                e1.record()
+                torch.cuda.synchronize()
+                if k >= args.warmup:
+                    ms.append(e0.elapsed_time(e1))
+            nom = torch.tensor([float(msw.stats()["nominal_points"])], device=dev)
+        tmu = torch.tensor([float(np.median(ms)) / 1e3], device=dev)
+        dist.all_reduce(tmu, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nom, op=dist.ReduceOp.SUM)
+        mu_block["config3_sharded"] = {"ms_per_iteration": 1e3 * float(tmu.item()),
+                                       "nominal_points_per_s": float(nom.item()) / float(tmu.item()),
+                                       "step": "sweep owned points + pack | NCCL all-gather | assemble + deltas",
+                                       "l2": "flushed before every timed step"}
     sys.stdout.flush()
     os.dup2(saved_stdout, 1)
     os.close(saved_stdout)

@@ -25,7 +25,7 @@ from . import _native as nat
 from .mu_grid import VERTICES, MuGrid, MuParams, build_mu_grid, grid_for
 
 __all__ = ["MuIterationRecord", "MuSolution", "MuSweeper", "solve_mu", "iterate_mu_once", "solve_mu_batch",
-           "solve_mu_batch_sharded", "owned_mus", "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
+           "solve_mu_batch_sharded", "solve_mu_sharded", "owned_mus", "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
 
 
 @dataclass(frozen=True)
@@ -204,6 +204,69 @@ def solve_mu_batch(mus, params: MuParams | None = None, grid: MuGrid | None = No
         for m in mus:
             out.append(sw.solve(replace(params, mu=float(m)), history=history))
     return out
+
+
+def solve_mu_sharded(params: MuParams | None = None, grid: MuGrid | None = None, a0=None, b0=None, c0=None,
+                     rank: int | None = None, world: int | None = None, device: int | None = None,
+                     gather=None) -> MuSolution:
+    """Config 3 with the external points sharded over the ranks of a
+    torch.distributed job (rank r owns points r, r + W, ...): per iteration
+    each GPU sweeps its points, the compact [3][ceil(N/W)] complex results
+    are all-gathered (NCCL), and every rank rebuilds the full iterate with
+    the relaxation blend and the max-norm deltas on the device; the stop
+    rule and history are the single-GPU solve's, and the result is bitwise
+    the single-GPU solve's (a point's reduction never depends on the owner).
+    `gather(out[W,3,per,2], buf[3,per,2])` defaults to all_gather_into_tensor."""
+    import ctypes
+    import math
+
+    import torch
+    import torch.distributed as dist
+    params = MuParams() if params is None else params
+    params.validate()
+    grid = grid_for(params) if grid is None else grid
+    if rank is None or world is None:
+        rank, world = dist.get_rank(), dist.get_world_size()
+    if device is None:
+        device = torch.cuda.current_device()
+    if gather is None:
+        def gather(out, buf):
+            dist.all_gather_into_tensor(out, buf)
+    dev = torch.device("cuda", device)
+    shape = (grid.n_s, grid.n_4)
+    n = grid.n_ext
+    per = math.ceil(n / world)
+    state = [torch.from_numpy(_state(x, shape, d).reshape(-1)).to(dev) for x, d in ((a0, 1.0), (b0, 0.3), (c0, 1.0))]
+    send = torch.zeros((3, per, 2), dtype=torch.float64, device=dev)
+    recv = torch.zeros((world, 3, per, 2), dtype=torch.float64, device=dev)
+    delta = torch.zeros(3, dtype=torch.float64, device=dev)
+    lib = nat.load()
+    cp = _c_params(params)
+    hist = [MuIterationRecord(0, float("nan"), float("nan"), float("nan"))]
+    with MuSweeper(grid, params, device, row_start=rank, row_stride=world) as sw:
+        err = nat.DseErr()
+        st = torch.cuda.current_stream(dev).cuda_stream
+        nat.raise_for(lib.dse_mu_solve_load(sw.handle, state[0].data_ptr(), state[1].data_ptr(),
+                                            state[2].data_ptr(), st, ctypes.byref(err)), err)
+        converged, n_it = False, params.max_iterations
+        for it in range(1, params.max_iterations + 1):
+            nat.raise_for(lib.dse_mu_sharded_sweep_pack(sw.handle, ctypes.byref(cp), send.data_ptr(), per, st,
+                                                        ctypes.byref(err)), err)
+            gather(recv, send)
+            nat.raise_for(lib.dse_mu_sharded_assemble(sw.handle, recv.data_ptr(), world, per, params.relaxation,
+                                                      delta.data_ptr(), st, ctypes.byref(err)), err)
+            d = delta.cpu().numpy()
+            nat.raise_for(lib.dse_mu_sharded_failure(sw.handle, st, ctypes.byref(err)), err)
+            hist.append(MuIterationRecord(it, float(d[0]), float(d[1]), float(d[2])))
+            if d[0] < params.xi and d[1] < params.xi and d[2] < params.xi:
+                converged, n_it = True, it
+                break
+        px = ctypes.c_void_p()
+        nat.raise_for(lib.dse_mu_sweeper_state(sw.handle, ctypes.byref(px)), nat.DseErr())
+        from .distributed import device_view
+        full = device_view(px.value, 3 * 2 * n, dev).cpu().numpy().view(np.complex128).reshape(3, *shape)
+    return MuSolution(A=full[0].copy(), B=full[1].copy(), C=full[2].copy(), iterations=n_it, converged=converged,
+                      history=hist, grid=grid, params=params)
 
 
 def owned_mus(mus, rank: int, world: int) -> list:

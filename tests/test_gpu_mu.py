@@ -140,3 +140,71 @@ def test_stats_count_points():
         st = sw.stats()
     assert st["nominal_points"] == g.nominal_points
     assert 0 < st["evaluated_points"] <= st["nominal_points"]
+
+
+def test_sharded_solve_world1_equals_solve():
+    """solve_mu_sharded (sweep+pack | gather | assemble+blend+deltas per
+    iteration) at world 1 is bitwise the on-device single-GPU solve."""
+    import torch
+
+    from paper_2012_03667_b200.finite_mu import solve_mu_sharded
+    p = MuParams(mu=0.2, vertex="bcb", max_iterations=200, relaxation=0.8, **SMALL)
+    g = grid_for(p)
+    ref = solve_mu(p, g)
+
+    def copy_gather(out, buf):
+        out[0].copy_(buf)
+
+    got = solve_mu_sharded(p, g, rank=0, world=1, device=0, gather=copy_gather)
+    assert got.iterations == ref.iterations and got.converged == ref.converged
+    for x, y in ((got.A, ref.A), (got.B, ref.B), (got.C, ref.C)):
+        assert np.array_equal(x.view(np.float64), y.view(np.float64))
+    assert [(r.n, r.delta_a, r.delta_b, r.delta_c) for r in got.history[1:]] == \
+        [(r.n, r.delta_a, r.delta_b, r.delta_c) for r in ref.history[1:]]
+    torch.cuda.synchronize()
+
+
+def test_sharded_iteration_world3_emulated():
+    """Three row-sharded sweepers (ranks run one after another on one GPU,
+    nothing waits on anything) + the stacked send buffers reproduce one
+    single-GPU sweep bitwise on every rank."""
+    import ctypes
+    import math
+
+    import torch
+
+    from paper_2012_03667_b200 import _native as nat
+    from paper_2012_03667_b200.distributed import device_view
+    from paper_2012_03667_b200.finite_mu import _c_params
+    p = MuParams(**SMALL)
+    g = grid_for(p)
+    A, B, C = _state(g, 6)
+    ref = iterate_mu_once(g, A, B, C, p)
+    W = 3
+    per = math.ceil(g.n_ext / W)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    lib = nat.load()
+    cp = _c_params(p)
+    tens = [torch.from_numpy(np.ascontiguousarray(x.reshape(-1))).to(dev) for x in (A, B, C)]
+    sws = [MuSweeper(g, p, row_start=r, row_stride=W) for r in range(W)]
+    sends = [torch.zeros((3, per, 2), dtype=torch.float64, device=dev) for _ in range(W)]
+    err = nat.DseErr()
+    for sw, send in zip(sws, sends):
+        nat.raise_for(lib.dse_mu_solve_load(sw.handle, *[t.data_ptr() for t in tens], st, ctypes.byref(err)), err)
+        nat.raise_for(lib.dse_mu_sharded_sweep_pack(sw.handle, ctypes.byref(cp), send.data_ptr(), per, st,
+                                                    ctypes.byref(err)), err)
+    recv = torch.stack(sends)
+    delta = torch.zeros(3, dtype=torch.float64, device=dev)
+    for sw in sws:
+        nat.raise_for(lib.dse_mu_sharded_assemble(sw.handle, recv.data_ptr(), W, per, 1.0, delta.data_ptr(), st,
+                                                  ctypes.byref(err)), err)
+        px = ctypes.c_void_p()
+        nat.raise_for(lib.dse_mu_sweeper_state(sw.handle, ctypes.byref(px)), nat.DseErr())
+        full = device_view(px.value, 6 * g.n_ext, dev).cpu().numpy().view(np.complex128).reshape(3, g.n_s, g.n_4)
+        for f in range(3):
+            assert np.array_equal(full[f].view(np.float64), ref[f].view(np.float64))
+        d = delta.cpu().numpy()
+        assert d[0] == np.max(np.abs(ref[0] - A))
+    for sw in sws:
+        sw.close()
