@@ -73,6 +73,10 @@ struct MuArgs {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+#ifndef DSE_MU_UNROLL
+#define DSE_MU_UNROLL 8  // config 3, bcb: unroll 2 5.46, 4 5.52, 8 5.35 ms; 3 CTAs/SM (80 regs) 5.51 ms
+#endif
+constexpr int kMuUnroll = DSE_MU_UNROLL;
 #ifndef DSE_MU_MINB
 #define DSE_MU_MINB 2  // CTAs per SM the register budget is cut for (A/B: scripts/mu_ab.sh)
 #endif
@@ -144,7 +148,7 @@ __device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, in
     const double c0 = fma(k4, k4, rc.P2 + Q2);
     const dse::ExpK ek{a.exp_c1, 0.0};
     double S0 = 0.0, S1 = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0;
-#pragma unroll 4
+#pragma unroll kMuUnroll
     for (int k = 0; k < a.K; ++k) {
         const double2 zk = zw[k];
         const double r = PQ * zk.x;
