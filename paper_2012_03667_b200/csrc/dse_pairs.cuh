@@ -40,6 +40,8 @@ constexpr int kPairsThreads = 256;
 #define DSE_PAIRS_UNROLL 8  // measured at config 2: 2 -> 0.368, 4 -> 0.356, 8 -> 0.351 ms
 #endif
 constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
+// (two accumulator sets for even/odd angles ran 0.344 vs 0.339 ms: the loop
+// is FP64-pipe bound, not add-chain bound)
 // (an 11-bit exp table with a degree-3 polynomial ran 0.333 ms but put a
 // config-2 random-state sweep at 1.1e-12 of the oracle: kept at 8 bits, degree 4)
 
