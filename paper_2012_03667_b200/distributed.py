@@ -29,7 +29,7 @@ from typing import Callable
 
 import numpy as np
 
-from .errors import ParameterError
+from .errors import ExecutionEnvironmentError, ParameterError
 
 __all__ = ["owned_rows", "ShardedLoop", "solve_sharded", "iterate_once_sharded", "bench_main"]
 
@@ -275,14 +275,25 @@ class P2PShardedStep:
         # (the push of e+2 waits for everyone's push of e+1, which follows
         # their assemble of e in stream order)
         self._slot = world * 2 * self.per
-        for nbytes in (2 * self._slot * 8, 64):
-            ptr = ctypes.c_void_p()
-            h = ctypes.create_string_buffer(64)
-            nat.raise_for(self._lib.dse_p2p_alloc(device, nbytes, ctypes.byref(ptr), h, ctypes.byref(err)), err)
-            self._own.append(ptr.value)
-            handles.append(h.raw)
-        everyone = exchange(tuple(handles))
+        # collective-safe construction: every rank makes exactly one
+        # `exchange` call whatever fails locally, and an allocation or
+        # mapping failure is reported through it (no rank is left waiting)
+        local_error = None
+        try:
+            for nbytes in (2 * self._slot * 8, 64):
+                ptr = ctypes.c_void_p()
+                h = ctypes.create_string_buffer(64)
+                nat.raise_for(self._lib.dse_p2p_alloc(device, nbytes, ctypes.byref(ptr), h, ctypes.byref(err)), err)
+                self._own.append(ptr.value)
+                handles.append(h.raw)
+        except Exception as exc:  # noqa: BLE001
+            local_error = f"{type(exc).__name__}: {exc}"
+        everyone = exchange((local_error, tuple(handles)))
+        bad = [f"rank {q}: {e}" for q, (e, _) in enumerate(everyone) if e is not None]
         self._mapped = []
+        if bad:
+            self.close()
+            raise ExecutionEnvironmentError("peer-memory setup failed on " + "; ".join(bad))
         recv, flags = [], []
         for q in range(world):
             if q == rank:
@@ -292,8 +303,8 @@ class P2PShardedStep:
             got = []
             for k in range(2):
                 ptr = ctypes.c_void_p()
-                nat.raise_for(self._lib.dse_p2p_open(device, everyone[q][k], ctypes.byref(ptr), ctypes.byref(err)),
-                              err)
+                nat.raise_for(self._lib.dse_p2p_open(device, everyone[q][1][k], ctypes.byref(ptr),
+                                                     ctypes.byref(err)), err)
                 got.append(ptr.value)
                 self._mapped.append(ptr.value)
             recv.append(got[0])
@@ -400,31 +411,45 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
     exchanger = None
     p2p_note = "disabled (DSE_P2P=0)"
     if os.environ.get("DSE_P2P", "1") != "0":
+        # every rank runs the same collectives on every path: the IPC exchange
+        # (inside P2PShardedStep, which reports local failures through it) and
+        # one all_reduce of the local verdict
+        def exchange(obj):
+            out = [None] * world
+            dist.all_gather_object(out, obj)
+            return out
+        ok_here, why = 0, "setup"
         try:
-            def exchange(obj):
-                out = [None] * world
-                dist.all_gather_object(out, obj)
-                return out
             exchanger = P2PShardedStep(sw, grid.n_ext, world, rank, local, dev, exchange)
-            fused.load(a, b, sp)
-            fused.step(sp)
-            ref = torch.cat([device_view(state_ptr[0], grid.n_ext, dev), device_view(state_ptr[1], grid.n_ext, dev)])
-            ref = ref.clone()
-            exchanger.load(a, b, sp)
-            exchanger.step(sp)
-            got = torch.cat([device_view(state_ptr[0], grid.n_ext, dev), device_view(state_ptr[1], grid.n_ext, dev)])
-            torch.cuda.synchronize()
-            ok_here = bool(torch.equal(got, ref)) and int(exchanger.timed_out.item()) == 0
-            flag = torch.tensor([1 if ok_here else 0], device=dev)
+        except Exception as exc:  # noqa: BLE001 -- every rank raised (the exchange told them)
+            exchanger, why = None, f"{type(exc).__name__}: {str(exc)[:120]}"
+        if exchanger is not None:
+            try:
+                fused.load(a, b, sp)
+                fused.step(sp)
+                ref = torch.cat([device_view(state_ptr[0], grid.n_ext, dev),
+                                 device_view(state_ptr[1], grid.n_ext, dev)]).clone()
+                exchanger.load(a, b, sp)
+                exchanger.step(sp)
+                got = torch.cat([device_view(state_ptr[0], grid.n_ext, dev),
+                                 device_view(state_ptr[1], grid.n_ext, dev)])
+                torch.cuda.synchronize()
+                ok_here = int(bool(torch.equal(got, ref)) and int(exchanger.timed_out.item()) == 0)
+                why = "peer-memory step disagreed with the NCCL step or timed out on some rank"
+            except Exception as exc:  # noqa: BLE001
+                ok_here, why = 0, f"{type(exc).__name__}: {str(exc)[:120]}"
+            flag = torch.tensor([ok_here], device=dev)
             dist.all_reduce(flag, op=dist.ReduceOp.MIN)
             if int(flag.item()) == 1:
                 p2p_note = "peer-memory all-gather fused into the sweep (validated bitwise vs the NCCL step)"
             else:
-                p2p_note = "fallback to NCCL: peer-memory step disagreed or timed out on some rank"
+                p2p_note = f"fallback to NCCL: {why}"
+                torch.cuda.synchronize()
+                dist.barrier()
+                exchanger.close()
                 exchanger = None
-        except Exception as exc:  # noqa: BLE001
-            p2p_note = f"fallback to NCCL: {type(exc).__name__}: {str(exc)[:120]}"
-            exchanger = None
+        else:
+            p2p_note = f"fallback to NCCL: {why}"
     stepper = exchanger if exchanger is not None else fused
 
     def step():
