@@ -89,11 +89,12 @@ def test_solve_numerical_failure_raises():
     assert ei.value.iteration == 1 and ei.value.row is not None
 
 
-def test_moments_batch_equals_standalone():
-    """Batched solves with the moments arithmetic (concurrent per-solve
-    sweepers) equal the standalone solves bitwise."""
+@pytest.mark.parametrize("vname", ["indexed-gpu-moments", "indexed-gpu-pairs"])
+def test_moments_batch_equals_standalone(vname):
+    """Batched solves with the moments / pairs arithmetic (concurrent
+    per-solve sweepers) equal the standalone solves bitwise."""
     g = golden_grid("c0")
-    v = p.VARIANTS["indexed-gpu-moments"]
+    v = p.VARIANTS[vname]
     prms = [p.ModelParams(N=128, m_rad=128, m_ang=64, xi=1e-10, max_iterations=5000, D=D) for D in (0.5, 0.6)]
     batch = p.solve_batch(prms, v, grid=g, b0s=[np.full(g.n_ext, 0.3)] * 2)
     for prm, sb in zip(prms, batch):
@@ -102,7 +103,8 @@ def test_moments_batch_equals_standalone():
         assert np.array_equal(sb.A, s1.A) and np.array_equal(sb.B, s1.B)
 
 
-@pytest.mark.parametrize("arith", [p.Arithmetic.EXACT, p.Arithmetic.FAST, p.Arithmetic.MOMENTS])
+@pytest.mark.parametrize("arith", [p.Arithmetic.EXACT, p.Arithmetic.FAST, p.Arithmetic.MOMENTS,
+                                   p.Arithmetic.PAIRS])
 def test_load_resume_status_protocol(arith):
     """dse_solve_load + dse_solve_resume on a fresh sweeper (no sweep/solve
     first): a clean run checks clean, a non-finite state reports the reference
