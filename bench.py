@@ -605,7 +605,47 @@ def mu_bench(p, torch, dev, flush, args, peak, no_cpu):
                 "h2d_bytes": 3 * 16 * g.n_ext, "d2h_bytes": 3 * 16 * g.n_ext + 32 * (sol_e.iterations + 1)},
         "M_ir": str(sol.mass[0, g.n_4 // 2]),
     }
+    # moments mode: the five angular moments of every evaluated pair built
+    # once (grid + omega only), contracted each iteration -- bitwise the direct
+    # results (tests/test_gpu_mu*.py); reported as time to solution, not as
+    # integrand points/s (a moment iteration does not evaluate the points)
+    from dataclasses import replace as _replace
+    pmo = _replace(prm, mode="moments")
+    with MuSweeper(g, pmo) as sw:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sw.solve(_replace(pmo, max_iterations=1), history=False)  # builds the table (+ one iteration)
+        build_wall = time.perf_counter() - t0
+        stream = torch.cuda.Stream(device=dev)
+        sp = stream.cuda_stream
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        with torch.cuda.stream(stream):
+            for e0, e1 in ev:
+                sw.load_device(A0.data_ptr(), B0.data_ptr(), C0.data_ptr(), sp)
+                flush.fill_(1)
+                e0.record(stream)
+                sw.resume(1, sp)
+                e1.record(stream)
+            stream.synchronize()
+        t_mo = float(np.median([e0.elapsed_time(e1) for e0, e1 in ev])) / 1e3
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        smo = sw.solve(pmo)
+        e1.record()
+        torch.cuda.synchronize()
+        tts_mo = e0.elapsed_time(e1) / 1e3
+    out["config3"]["moments_mode"] = {
+        "ms_per_iteration": 1e3 * t_mo, "table_build_wall_s": build_wall,
+        "table_bytes": int(st["evaluated_points"] // prm.m_ang * 5 * 8),
+        "time_to_solution": {"iterations": smo.iterations, "converged": smo.converged, "seconds_device": tts_mo,
+                             "seconds_with_build": tts_mo + build_wall},
+        "bitwise_equal_to_direct": bool(np.array_equal(smo.A, sol.A) and np.array_equal(smo.B, sol.B)),
+    }
     mus = [0.4 * (k + 0.5) / 32 for k in range(32)]
+    t0 = time.perf_counter()
+    sols_mo = solve_mu_batch(mus, pmo, g)
+    t4mo = time.perf_counter() - t0
     t0 = time.perf_counter()
     sols = solve_mu_batch(mus, prm, g)
     t4 = time.perf_counter() - t0
@@ -613,7 +653,12 @@ def mu_bench(p, torch, dev, flush, args, peak, no_cpu):
                       "seconds_per_solve": t4 / len(mus), "iterations": [s.iterations for s in sols],
                       "converged": int(sum(s.converged for s in sols)),
                       "nominal_points_per_s": st["nominal_points"] * sum(s.iterations for s in sols) / t4,
-                      "layout": "one sweeper, 32 on-device solves back to back on 1 GPU (replicas; 4 per GPU at 8)"}
+                      "layout": "one sweeper, 32 on-device solves back to back on 1 GPU (replicas; 4 per GPU at 8)",
+                      "moments_mode": {"seconds": t4mo, "solves_per_s": len(mus) / t4mo,
+                                       "seconds_per_solve": t4mo / len(mus),
+                                       "iterations_equal_direct": [s.iterations for s in sols_mo] ==
+                                                                  [s.iterations for s in sols],
+                                       "note": "one moment table built once, shared by the 32 mu values"}}
     if not no_cpu:
         rate, info = mu_cpu_rate(float(os.environ.get("BENCH_MU_CPU_S", "8")))
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port",

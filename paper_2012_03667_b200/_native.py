@@ -56,7 +56,7 @@ class DseMuGrid(ctypes.Structure):
 
 class DseMuParams(ctypes.Structure):
     _fields_ = [(n, ctypes.c_double) for n in ("coeff", "omega", "m0", "z1", "mu", "xi", "relaxation")] + \
-               [("max_iterations", ctypes.c_int64), ("vertex", ctypes.c_int64)]
+               [("max_iterations", ctypes.c_int64), ("vertex", ctypes.c_int64), ("mode", ctypes.c_int64)]
 
 
 _LIB = None

@@ -69,6 +69,14 @@ struct MuArgs {
     double* hist;          // (cap+1) x 4 or null
     long long* evaluated;  // pairs evaluated (diagnostic; null = not counted)
     int it_begin, it_end, sweep_only, vertex;
+    // moments mode (DSE_MU_MODE_MOMENTS): per owned row r the exact-zero
+    // windows (rlo [r][m_s], roff [r][m_s + 1]) and the five angular moments
+    // of every evaluated pair, mom[m * mo_stride + mo_base[r] + f]
+    const int* mo_rlo;
+    const int* mo_roff;
+    const long long* mo_base;
+    double* mo_mom;
+    long long mo_stride;
 };
 
 constexpr int kThreads = 256;
@@ -135,15 +143,11 @@ struct RowC {
 // One (row, node) pair: angular moments, then the complex contraction.
 // acc[0..5] += (A, B, C channel) * meas * coeff / den (before the row's
 // division by |p|^2 and p~4).
-template <int V>
-__device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, int js, int j4,
-                                             const double2* __restrict__ zw, unsigned tbl, double acc[6]) {
-    const int j = js * a.m_4 + j4;
+// The five angular moments of one (row, node) pair, point by point.
+__device__ __forceinline__ void pair_moments(const MuArgs& a, const RowC& rc, int js, int j4,
+                                             const double2* __restrict__ zw, unsigned tbl, double mom[5]) {
     const double Qs = __ldg(a.Qs + js), Q2 = __ldg(a.Q2 + js), q4r = __ldg(a.q4 + j4);
     const double k4 = q4r - rc.p4r;
-    // node values first: their latency hides behind the angular loop
-    const double2* nb = a.NB + 4 * (size_t)j;
-    const double2 vA = nb[0], vB = nb[1], vC = nb[2], vR = nb[3];
     const double PQ = rc.P * Qs;
     const double c0 = fma(k4, k4, rc.P2 + Q2);
     const dse::ExpK ek{a.exp_c1, 0.0};
@@ -164,6 +168,22 @@ __device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, in
         T1 += t;
         T2 = fma(t, r, T2);
     }
+    mom[0] = S0;
+    mom[1] = S1;
+    mom[2] = T0;
+    mom[3] = T1;
+    mom[4] = T2;
+}
+
+// The complex contraction of a pair's moments; acc[0..5] += (A, B, C) * meas
+// * coeff / den (before the row's division by |p|^2 and p~4).
+template <int V>
+__device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, int js, int j4, const double2* vn,
+                                              const double mom[5], double acc[6]) {
+    const double Q2 = __ldg(a.Q2 + js), q4r = __ldg(a.q4 + j4);
+    const double k4 = q4r - rc.p4r;
+    const double S0 = mom[0], S1 = mom[1], T0 = mom[2], T1 = mom[3], T2 = mom[4];
+    const double2 vA = vn[0], vB = vn[1], vC = vn[2], vR = vn[3];
     const cplx Aq = C(vA.x, vA.y), Bq = C(vB.x, vB.y), Cq = C(vC.x, vC.y);
     const cplx q4t = C(q4r, a.mu);
     const cplx t4 = C(q4r + rc.p4r, 2.0 * a.mu);
@@ -244,6 +264,17 @@ __device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, in
     acc[4] += gC.x; acc[5] += gC.y;
 }
 
+template <int V>
+__device__ __forceinline__ void pair_contrib(const MuArgs& a, const RowC& rc, int js, int j4,
+                                             const double2* __restrict__ zw, unsigned tbl, double acc[6]) {
+    // node values first: their latency hides behind the angular loop
+    const double2* nb = a.NB + 4 * (size_t)(js * a.m_4 + j4);
+    const double2 vn[4] = {nb[0], nb[1], nb[2], nb[3]};
+    double mom[5];
+    pair_moments(a, rc, js, j4, zw, tbl, mom);
+    pair_contract<V>(a, rc, js, j4, vn, mom, acc);
+}
+
 __device__ __forceinline__ double hyp(double x, double y) { return hypot(x, y); }
 
 // relax * new + (1 - relax) * old per component, each operation rounded once
@@ -294,7 +325,144 @@ __global__ void __launch_bounds__(1024) mu_assemble_kernel(const double2* __rest
     }
 }
 
-template <int V>
+
+// The exact-zero windows of one row: per radial node js the evaluated q4
+// form one window around p4.  Fills rlo[m_s], roff[m_s + 1]
+// (shared) and returns the row's number of evaluated pairs.  all = evaluate
+// every pair (a non-finite node must reach the sums).
+template <class ScanT>
+__device__ int row_windows(const MuArgs& a, const RowC& rc, bool all, const double* q4s, int* rlo, int* roff,
+                           typename ScanT::TempStorage& scan_tmp, int& s_carry) {
+    const int tid = threadIdx.x;
+    if (tid == 0) s_carry = 0;
+    for (int base = 0; base < a.m_s; base += kThreads) {
+        const int js = base + tid;
+        int len = 0;
+        if (js < a.m_s) {
+            int lo = 0, hi = a.m_4;
+            if (!all) {
+                const double dPQ = rc.P - __ldg(a.Qs + js);
+                const double d2 = a.skip_k2 - dPQ * dPQ;
+                if (d2 < 0.0) {
+                    hi = 0;
+                } else {
+                    const double half = sqrt(d2) * (1.0 + 1e-12) + 1e-300;
+                    const double x0 = rc.p4r - half, x1 = rc.p4r + half;
+                    int l = 0, h = a.m_4;  // first q4 >= x0
+                    while (l < h) { const int mm = (l + h) >> 1; if (q4s[mm] < x0) l = mm + 1; else h = mm; }
+                    lo = l;
+                    h = a.m_4;             // first q4 > x1
+                    while (l < h) { const int mm = (l + h) >> 1; if (q4s[mm] <= x1) l = mm + 1; else h = mm; }
+                    hi = l;
+                }
+            }
+            len = max(hi - lo, 0);
+            rlo[js] = lo;
+        }
+        int ex;
+        __syncthreads();  // s_carry written
+        const int carry = s_carry;
+        ScanT(scan_tmp).ExclusiveSum(len, ex);
+        if (js < a.m_s) roff[js] = carry + ex;
+        __syncthreads();
+        if (tid == kThreads - 1) s_carry = carry + ex + len;
+    }
+    __syncthreads();
+    const int total = s_carry;
+    if (tid == 0) roff[a.m_s] = total;
+    __syncthreads();
+    return total;
+}
+
+// node js of flat pair index f: fixed-trip binary search over roff (the
+// warp's lanes stay converged through the pair body)
+__device__ __forceinline__ int node_of(const int* roff, int m_s, int top, int f) {
+    int js = 0;
+    for (int step = top >> 1; step > 0; step >>= 1) js = (js + step < m_s && roff[js + step] <= f) ? js + step : js;
+    return js;
+}
+
+__device__ __forceinline__ RowC row_consts(const MuArgs& a, const double2* Xin, int n_ext, int i) {
+    const int is = i / a.n_4, i4 = i - is * a.n_4;
+    RowC rc;
+    rc.P = a.P[is];
+    rc.P2 = a.P2[is];
+    rc.p4r = a.p4[i4];
+    rc.p4t = C(rc.p4r, a.mu);
+    const double2 va = Xin[i], vb = Xin[n_ext + i], vc = Xin[2 * n_ext + i];
+    rc.Ap = C(va.x, va.y);
+    rc.Bp = C(vb.x, vb.y);
+    rc.Cp = C(vc.x, vc.y);
+    return rc;
+}
+
+// Moments mode, pass 1: every owned row's windows (geometry only: P, p4,
+// the |q| and q4 nodes, omega) into the global tables and its pair count.
+__global__ void __launch_bounds__(kThreads) mu_windows_kernel(MuArgs a, int* rlo_g, int* roff_g, long long* tot) {
+    extern __shared__ __align__(16) double sm[];
+    double* q4s = sm;
+    int* rlo = reinterpret_cast<int*>(q4s + a.m_4);
+    int* roff = rlo + a.m_s;
+    using Scan = cub::BlockScan<int, kThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_carry;
+    for (int k = threadIdx.x; k < a.m_4; k += kThreads) q4s[k] = __ldg(a.q4 + k);
+    __syncthreads();
+    for (int r = blockIdx.x; r < a.n_rows; r += gridDim.x) {
+        const int i = a.row_start + r * a.row_stride;
+        const int is = i / a.n_4, i4 = i - is * a.n_4;
+        RowC rc{};
+        rc.P = a.P[is];
+        rc.P2 = a.P2[is];
+        rc.p4r = a.p4[i4];
+        const int total = row_windows<Scan>(a, rc, false, q4s, rlo, roff, scan_tmp, s_carry);
+        for (int js = threadIdx.x; js < a.m_s; js += kThreads) rlo_g[(size_t)r * a.m_s + js] = rlo[js];
+        for (int js = threadIdx.x; js <= a.m_s; js += kThreads) roff_g[(size_t)r * (a.m_s + 1) + js] = roff[js];
+        if (threadIdx.x == 0) tot[r] = total;
+        __syncthreads();
+    }
+}
+
+// Moments mode, pass 2: the five moments of every evaluated pair (the same
+// pair_moments as the direct sweep: the moments are bitwise those the direct
+// sweep forms every iteration).
+__global__ void __launch_bounds__(kThreads) mu_moments_build_kernel(MuArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    double* etbl = sm;
+    double2* zw = reinterpret_cast<double2*>(sm + (1 << dse::kExpTableBits));
+    int* roff = reinterpret_cast<int*>(zw + a.K);
+    for (int i = threadIdx.x; i < (1 << dse::kExpTableBits); i += kThreads) etbl[i] = __ldg(a.exp_tbl + i);
+    for (int k = threadIdx.x; k < a.K; k += kThreads) zw[k] = make_double2(__ldg(a.z + k), __ldg(a.wz + k));
+    __syncthreads();
+    const unsigned tbl = dse::smem_addr(etbl);
+    int top = 1;
+    while (top < a.m_s) top <<= 1;
+    for (int r = blockIdx.x; r < a.n_rows; r += gridDim.x) {
+        const int i = a.row_start + r * a.row_stride;
+        const int is = i / a.n_4, i4 = i - is * a.n_4;
+        RowC rc{};
+        rc.P = a.P[is];
+        rc.P2 = a.P2[is];
+        rc.p4r = a.p4[i4];
+        for (int js = threadIdx.x; js <= a.m_s; js += kThreads) roff[js] = a.mo_roff[(size_t)r * (a.m_s + 1) + js];
+        __syncthreads();
+        const int total = roff[a.m_s];
+        const long long base = a.mo_base[r];
+        for (int f0 = 0; f0 < total; f0 += kThreads) {
+            const int f = min(f0 + threadIdx.x, total - 1);
+            const int js = node_of(roff, a.m_s, top, f);
+            const int j4 = a.mo_rlo[(size_t)r * a.m_s + js] + (f - roff[js]);
+            __syncwarp();
+            double mom[5];
+            pair_moments(a, rc, js, j4, zw, tbl, mom);
+            if (f0 + threadIdx.x < total)
+                for (int q = 0; q < 5; ++q) a.mo_mom[q * a.mo_stride + base + f] = mom[q];
+        }
+        __syncthreads();
+    }
+}
+
+template <int V, bool MOM>
 __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs a) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) double smem[];
@@ -336,60 +504,28 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
             __syncthreads();
             if (r >= (unsigned)a.n_rows) break;
             const int i = a.row_start + (int)r * a.row_stride;
-            const int is = i / a.n_4, i4 = i - is * a.n_4;
-            RowC rc;
-            rc.P = a.P[is];
-            rc.P2 = a.P2[is];
-            rc.p4r = a.p4[i4];
-            rc.p4t = C(rc.p4r, a.mu);
+            const RowC rc = row_consts(a, Xin, n_ext, i);
             const double2 va = Xin[i], vb = Xin[n_ext + i], vc = Xin[2 * n_ext + i];
-            rc.Ap = C(va.x, va.y);
-            rc.Bp = C(vb.x, vb.y);
-            rc.Cp = C(vc.x, vc.y);
-            // Pairs whose exp(-k^2/w^2) underflows at every angle are exact
-            // zeros of the sum: per radial node js the evaluated q4
-            // form one window around p4.  Flatten the windows and deal the
-            // pairs round-robin, so every thread gets the same count.
             const bool all = a.nonfinite[cur] != 0;  // a non-finite node must reach the sum
-            using Scan = cub::BlockScan<int, kThreads>;
-            __shared__ typename Scan::TempStorage scan_tmp;
-            if (tid == 0) s_carry = 0;
-            for (int base = 0; base < a.m_s; base += kThreads) {
-                const int js = base + tid;
-                int len = 0;
-                if (js < a.m_s) {
-                    int lo = 0, hi = a.m_4;
-                    if (!all) {
-                        const double dPQ = rc.P - __ldg(a.Qs + js);
-                        const double d2 = a.skip_k2 - dPQ * dPQ;
-                        if (d2 < 0.0) {
-                            hi = 0;
-                        } else {
-                            const double half = sqrt(d2) * (1.0 + 1e-12) + 1e-300;
-                            const double x0 = rc.p4r - half, x1 = rc.p4r + half;
-                            int l = 0, h = a.m_4;  // first q4 >= x0
-                            while (l < h) { const int m = (l + h) >> 1; if (q4s[m] < x0) l = m + 1; else h = m; }
-                            lo = l;
-                            h = a.m_4;             // first q4 > x1
-                            while (l < h) { const int m = (l + h) >> 1; if (q4s[m] <= x1) l = m + 1; else h = m; }
-                            hi = l;
-                        }
-                    }
-                    len = max(hi - lo, 0);
-                    rlo[js] = lo;
+            int total;
+            if (MOM) {
+                // precomputed windows; a non-finite node fails the lowest owned
+                // row directly (every row's reference sum contains it), the
+                // location comes from the direct per-point pass
+                if (all) {
+                    if (tid == 0) atomicMin(a.err + cur, (unsigned long long)a.row_start);
+                    continue;
                 }
-                int ex;
-                __syncthreads();  // s_carry written
-                const int carry = s_carry;
-                Scan(scan_tmp).ExclusiveSum(len, ex);
-                if (js < a.m_s) roff[js] = carry + ex;
+                for (int js = tid; js < a.m_s; js += kThreads) rlo[js] = __ldg(a.mo_rlo + (size_t)r * a.m_s + js);
+                for (int js = tid; js <= a.m_s; js += kThreads)
+                    roff[js] = __ldg(a.mo_roff + (size_t)r * (a.m_s + 1) + js);
                 __syncthreads();
-                if (tid == kThreads - 1) s_carry = carry + ex + len;
+                total = roff[a.m_s];
+            } else {
+                using Scan = cub::BlockScan<int, kThreads>;
+                __shared__ typename Scan::TempStorage scan_tmp;
+                total = row_windows<Scan>(a, rc, all, q4s, rlo, roff, scan_tmp, s_carry);
             }
-            __syncthreads();
-            const int total = s_carry;
-            if (tid == 0) roff[a.m_s] = total;
-            __syncthreads();
             double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             // the warp's lanes stay converged through the pair body: the node
             // of flat index f is found by a fixed-trip binary search over the
@@ -397,14 +533,22 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
             // lanes active on average)
             int top = 1;
             while (top < a.m_s) top <<= 1;
+            const long long mbase = MOM ? __ldg(a.mo_base + r) : 0;
             for (int f0 = 0; f0 < total; f0 += kThreads) {
                 const int f = min(f0 + tid, total - 1);
-                int js = 0;
-                for (int step = top >> 1; step > 0; step >>= 1)
-                    js = (js + step < a.m_s && roff[js + step] <= f) ? js + step : js;
+                const int js = node_of(roff, a.m_s, top, f);
+                const int j4 = rlo[js] + (f - roff[js]);
                 __syncwarp();
                 double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-                pair_contrib<V>(a, rc, js, rlo[js] + (f - roff[js]), zw, tbl, part);
+                if (MOM) {
+                    const double2* nb = a.NB + 4 * (size_t)(js * a.m_4 + j4);
+                    const double2 vn[4] = {nb[0], nb[1], nb[2], nb[3]};
+                    double mom[5];
+                    for (int q = 0; q < 5; ++q) mom[q] = __ldcs(a.mo_mom + q * a.mo_stride + mbase + f);
+                    pair_contract<V>(a, rc, js, j4, vn, mom, part);
+                } else {
+                    pair_contrib<V>(a, rc, js, j4, zw, tbl, part);
+                }
                 if (f0 + tid < total)
                     for (int c = 0; c < 6; ++c) acc[c] += part[c];
             }
@@ -562,13 +706,21 @@ struct dse_mu_sweeper {
     size_t smem = 0;
     long long it_next = 0;
     long long evaluated_pairs = -1;
+    // moments mode tables (built on first use; geometry only, shared by every mu)
+    int* d_mo_rlo = nullptr;
+    int* d_mo_roff = nullptr;
+    long long* d_mo_base = nullptr;
+    double* d_mo_mom = nullptr;
+    long long mo_total = -1;
+    bool mo_mode = false;  // the current call runs the moments kernel
 };
 
 namespace {
 
 int mu_check_params(const dse_mu_params* p, dse_err* err) {
     if (!(p->omega > 0.0) || !(p->coeff >= 0.0) || !(p->xi > 0.0) || !(p->relaxation > 0.0 && p->relaxation <= 1.0) ||
-        p->max_iterations < 1 || !(p->mu >= 0.0) || !std::isfinite(p->mu) || p->vertex < 0 || p->vertex > 2)
+        p->max_iterations < 1 || !(p->mu >= 0.0) || !std::isfinite(p->mu) || p->vertex < 0 || p->vertex > 2 ||
+        p->mode < 0 || p->mode > 1)
         return fail(err, DSE_EPARAM, "finite-mu parameters out of range");
     return DSE_OK;
 }
@@ -592,16 +744,82 @@ mu::MuArgs mu_make_args(dse_mu_sweeper* s, const dse_mu_params& p, int it_begin,
     a.evaluated = count ? s->d_eval : nullptr;
     a.it_begin = it_begin; a.it_end = it_end; a.sweep_only = sweep_only ? 1 : 0;
     a.vertex = (int)p.vertex;
+    a.mo_rlo = s->d_mo_rlo; a.mo_roff = s->d_mo_roff; a.mo_base = s->d_mo_base; a.mo_mom = s->d_mo_mom;
+    a.mo_stride = s->mo_total > 0 ? s->mo_total : 0;
     return a;
 }
 
-const void* mu_kernel_ptr(int v) {
-    if (v == DSE_MU_VERTEX_BC1) return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BC1>;
-    if (v == DSE_MU_VERTEX_BCB) return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BCB>;
-    return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BC>;
+const void* mu_kernel_ptr(int v, bool mom = false) {
+    if (mom) {
+        if (v == DSE_MU_VERTEX_BC1) return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BC1, true>;
+        if (v == DSE_MU_VERTEX_BCB) return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BCB, true>;
+        return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BC, true>;
+    }
+    if (v == DSE_MU_VERTEX_BC1) return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BC1, false>;
+    if (v == DSE_MU_VERTEX_BCB) return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BCB, false>;
+    return (const void*)mu::mu_solve_kernel<DSE_MU_VERTEX_BC, false>;
+}
+
+// Moments mode: the windows and the five angular moments of every evaluated
+// pair of the owned rows, once per sweeper (they depend on the grid and
+// omega only, so every mu of a config-4 sweep reuses them).
+int mu_build_moments(dse_mu_sweeper* s, const dse_mu_params& p, dse_err* err) {
+    if (s->mo_total >= 0) return DSE_OK;
+    const size_t R = (size_t)s->n_rows, ms = (size_t)s->m_s;
+    CUDA_TRY(cudaMalloc(&s->d_mo_rlo, R * ms * sizeof(int)));
+    CUDA_TRY(cudaMalloc(&s->d_mo_roff, R * (ms + 1) * sizeof(int)));
+    CUDA_TRY(cudaMalloc(&s->d_mo_base, R * sizeof(long long)));
+    long long* d_tot = nullptr;
+    CUDA_TRY(cudaMalloc(&d_tot, R * sizeof(long long)));
+    mu::MuArgs a = mu_make_args(s, p, 0, 0, false, true, false);
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+    const size_t sm1 = (size_t)s->m_4 * sizeof(double) + (2 * ms + 2) * sizeof(int);
+    CUDA_TRY(cudaFuncSetAttribute((const void*)mu::mu_windows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sm1));
+    mu::mu_windows_kernel<<<std::max(1, std::min((int)R, 4 * sms)), mu::kThreads, sm1, s->stream>>>(
+        a, s->d_mo_rlo, s->d_mo_roff, d_tot);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    std::vector<long long> tot(R), base(R);
+    CUDA_TRY(cudaMemcpyAsync(tot.data(), d_tot, R * sizeof(long long), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    cudaFree(d_tot);
+    long long sum = 0;
+    for (size_t r = 0; r < R; ++r) {
+        base[r] = sum;
+        sum += tot[r];
+    }
+    CUDA_TRY(cudaMemcpyAsync(s->d_mo_base, base.data(), R * sizeof(long long), cudaMemcpyHostToDevice, s->stream));
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    if ((size_t)std::max(sum, 1ll) * 5 * sizeof(double) > free_b)
+        return fail(err, DSE_EENV, "moment table of %lld pairs does not fit in device memory", sum);
+    CUDA_TRY(cudaMalloc(&s->d_mo_mom, (size_t)std::max(sum, 1ll) * 5 * sizeof(double)));
+    s->mo_total = std::max(sum, 1ll);
+    a = mu_make_args(s, p, 0, 0, false, true, false);
+    const size_t sm2 = ((1 << dse::kExpTableBits) + 2 * (size_t)s->K) * sizeof(double) + (ms + 1) * sizeof(int);
+    CUDA_TRY(cudaFuncSetAttribute((const void*)mu::mu_moments_build_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)mu::mu_moments_build_kernel,
+                                                          mu::kThreads, sm2));
+    mu::mu_moments_build_kernel<<<std::max(1, std::min((int)R, std::max(per_sm, 1) * sms)), mu::kThreads, sm2,
+                                  s->stream>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return DSE_OK;
+}
+
+// select the kernel family of this call; build the moment table on first use
+int mu_prepare(dse_mu_sweeper* s, const dse_mu_params& p, dse_err* err) {
+    s->mo_mode = p.mode == DSE_MU_MODE_MOMENTS;
+    return s->mo_mode ? mu_build_moments(s, p, err) : DSE_OK;
 }
 
 int mu_launch(dse_mu_sweeper* s, const mu::MuArgs& a, bool reset, dse_err* err) {
+    if (s->mo_mode && !a.mo_mom) return fail(err, DSE_EENV, "moments mode without a moment table");
     if (reset) {
         mu::mu_reset_kernel<<<1, 32, 0, s->stream>>>(s->d_ctr, s->d_err, s->d_status, s->d_nonfinite);
         CUDA_TRY(cudaGetLastError());
@@ -609,7 +827,7 @@ int mu_launch(dse_mu_sweeper* s, const mu::MuArgs& a, bool reset, dse_err* err) 
     }
     mu::MuArgs b = a;
     void* args[] = {&b};
-    CUDA_TRY(cudaLaunchCooperativeKernel(mu_kernel_ptr(a.vertex), dim3(s->blocks), dim3(mu::kThreads), args,
+    CUDA_TRY(cudaLaunchCooperativeKernel(mu_kernel_ptr(a.vertex, a.mo_mom != nullptr && s->mo_mode), dim3(s->blocks), dim3(mu::kThreads), args,
                                          s->smem, s->stream));
     g_launches.fetch_add(1);
     return DSE_OK;
@@ -725,12 +943,14 @@ int dse_mu_sweeper_create(const dse_mu_grid* g, const dse_mu_params* p, int devi
     s->smem = (size_t)((1 << dse::kExpTableBits) + 2 * s->K + mu::kWarps * 6 + s->m_4) * sizeof(double) +
               (size_t)(2 * s->m_s + 2) * sizeof(int);
     int per_sm = 1 << 30, sms = 0;
-    for (int v : {DSE_MU_VERTEX_BC, DSE_MU_VERTEX_BC1, DSE_MU_VERTEX_BCB}) {
-        MU_TRY(cudaFuncSetAttribute(mu_kernel_ptr(v), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
-        int n = 0;
-        MU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mu_kernel_ptr(v), mu::kThreads, s->smem));
-        per_sm = std::min(per_sm, n);
-    }
+    for (int v : {DSE_MU_VERTEX_BC, DSE_MU_VERTEX_BC1, DSE_MU_VERTEX_BCB})
+        for (bool mom : {false, true}) {
+            MU_TRY(cudaFuncSetAttribute(mu_kernel_ptr(v, mom), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)s->smem));
+            int n = 0;
+            MU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mu_kernel_ptr(v, mom), mu::kThreads, s->smem));
+            per_sm = std::min(per_sm, n);
+        }
     MU_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     if (per_sm < 1) return bail(fail(err, DSE_EENV, "finite-mu kernel does not fit on an SM"));
     s->blocks = per_sm * sms;
@@ -749,7 +969,8 @@ int dse_mu_sweeper_destroy(dse_mu_sweeper* s) {
     for (void* p : {(void*)s->d_P, (void*)s->d_P2, (void*)s->d_p4, (void*)s->d_Qs, (void*)s->d_Q2, (void*)s->d_q4,
                     (void*)s->d_ms, (void*)s->d_m4, (void*)s->d_z, (void*)s->d_wz, (void*)s->d_etbl,
                     (void*)s->d_brk_s, (void*)s->d_brk_4, (void*)s->d_X, (void*)s->d_NB, (void*)s->d_bmax,
-                    (void*)s->d_ctr, (void*)s->d_err, (void*)s->d_status, (void*)s->d_eval, (void*)s->d_hist, (void*)s->d_nonfinite})
+                    (void*)s->d_ctr, (void*)s->d_err, (void*)s->d_status, (void*)s->d_eval, (void*)s->d_hist, (void*)s->d_nonfinite,
+                    (void*)s->d_mo_rlo, (void*)s->d_mo_roff, (void*)s->d_mo_base, (void*)s->d_mo_mom})
         if (p) cudaFree(p);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;
@@ -783,6 +1004,8 @@ int dse_mu_solve(dse_mu_sweeper* s, const dse_mu_params* params, double* A, doub
         s->hist_cap = cap + 1;
     }
     rc = mu_put_state(s, A, B, C_, err);
+    if (rc) return rc;
+    rc = mu_prepare(s, p, err);
     if (rc) return rc;
     const bool count = s->evaluated_pairs < 0;
     if (count) CUDA_TRY(cudaMemsetAsync(s->d_eval, 0, sizeof(long long), s->stream));
@@ -828,6 +1051,8 @@ int dse_mu_sweep(dse_mu_sweeper* s, const dse_mu_params* params, const double* A
     const size_t ne = (size_t)s->n_s * s->n_4;
     // rows not owned keep their input value in the output buffer
     CUDA_TRY(cudaMemcpyAsync(s->d_X + 3 * ne, s->d_X, 3 * ne * sizeof(double2), cudaMemcpyDeviceToDevice, s->stream));
+    rc = mu_prepare(s, p, err);
+    if (rc) return rc;
     mu::MuArgs a = mu_make_args(s, p, 0, 1, false, true, false);
     rc = mu_launch(s, a, true, err);
     if (rc) return rc;
@@ -868,6 +1093,8 @@ int dse_mu_solve_resume(dse_mu_sweeper* s, int64_t n_iterations, uintptr_t strea
     ok(err);
     if (!s || n_iterations < 1) return fail(err, DSE_EPARAM, "bad argument");
     CUDA_TRY(cudaSetDevice(s->device));
+    int rc0 = mu_prepare(s, s->prm, err);
+    if (rc0) return rc0;
     cudaStream_t keep = s->stream;
     s->stream = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     mu::MuArgs a = mu_make_args(s, s->prm, (int)s->it_next, (int)(s->it_next + n_iterations), false, true, false);
@@ -887,6 +1114,7 @@ int dse_mu_interp(dse_mu_sweeper* s, const double* F, double* out, dse_err* err)
     if (rc) return rc;
     // one sweep-only launch with zero iterations does not build nodes; run the
     // node phase through a 1-iteration sweep on a copy and read NB[.][0]
+    s->mo_mode = false;
     mu::MuArgs a = mu_make_args(s, s->prm, 0, 1, false, true, false);
     rc = mu_launch(s, a, true, err);
     if (rc) return rc;
@@ -910,6 +1138,8 @@ int dse_mu_sharded_sweep_pack(dse_mu_sweeper* s, const dse_mu_params* params, do
     if (rc) return rc;
     p.relaxation = 1.0;  // the blend is applied at assembly
     CUDA_TRY(cudaSetDevice(s->device));
+    rc = mu_prepare(s, p, err);
+    if (rc) return rc;
     cudaStream_t keep = s->stream;
     s->stream = (cudaStream_t)stream;  // 0 = the legacy default stream (CUDA convention)
     mu::MuArgs a = mu_make_args(s, p, 0, 1, false, true, false);

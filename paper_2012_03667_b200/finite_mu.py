@@ -22,7 +22,7 @@ from dataclasses import dataclass, field, replace
 import numpy as np
 
 from . import _native as nat
-from .mu_grid import VERTICES, MuGrid, MuParams, build_mu_grid, grid_for
+from .mu_grid import MODES, VERTICES, MuGrid, MuParams, build_mu_grid, grid_for
 
 __all__ = ["MuIterationRecord", "MuSolution", "MuSweeper", "solve_mu", "iterate_mu_once", "solve_mu_batch",
            "solve_mu_batch_sharded", "solve_mu_sharded", "owned_mus", "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
@@ -56,7 +56,7 @@ class MuSolution:
 def _c_params(p: MuParams) -> nat.DseMuParams:
     return nat.DseMuParams(coeff=p.interaction_coeff, omega=p.omega, m0=p.m0, z1=p.z1, mu=p.mu, xi=p.xi,
                            relaxation=p.relaxation, max_iterations=int(p.max_iterations),
-                           vertex=VERTICES.index(p.vertex))
+                           vertex=VERTICES.index(p.vertex), mode=MODES.index(p.mode))
 
 
 def _state(x, shape, default) -> np.ndarray:

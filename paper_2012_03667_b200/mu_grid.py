@@ -38,6 +38,7 @@ __all__ = ["MuParams", "MuGrid", "build_mu_grid", "mu_bracket_indices", "THREE_V
 # d^4q/(2 pi)^4 = (1/(2 pi)^4) dq4 |q|^2 d|q| (2 pi) dz  ->  1/(8 pi^3)
 THREE_VOLUME_COEFF = 1.0 / (8.0 * np.pi**3)
 VERTICES = ("bc", "bc1", "bcb")  # order = DSE_MU_VERTEX_* codes
+MODES = ("direct", "moments")    # order = DSE_MU_MODE_* codes
 _COINCIDENCE_RTOL = 1e-12
 
 
@@ -72,9 +73,13 @@ class MuParams:
     # Ball-Chiu vertex (diverges under successive approximation on these grids,
     # DESIGN.md); "bc1" the Sigma structure only
     vertex: str = "bcb"
+    # "direct": every integrand point every iteration; "moments": the angular
+    # moments built once per grid (shared by every mu) and contracted per iteration
+    mode: str = "direct"
 
     def validate(self) -> None:
         checks = [
+            ("mode", self.mode in MODES),
             ("vertex", self.vertex in VERTICES),
             ("D", self.D >= 0.0),
             ("omega", self.omega > 0.0),

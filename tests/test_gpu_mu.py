@@ -208,3 +208,48 @@ def test_sharded_iteration_world3_emulated():
         assert d[0] == np.max(np.abs(ref[0] - A))
     for sw in sws:
         sw.close()
+
+
+@pytest.mark.parametrize("vertex", ["bcb", "bc1", "bc"])
+def test_moments_mode_bitwise_equals_direct(vertex):
+    """Moments mode (angular moments built once per grid, contracted every
+    iteration) is the direct sweep's own arithmetic: bitwise equal, for one
+    sweep and for a whole solve (iterations, state, history)."""
+    A, B, C = None, None, None
+    p = MuParams(mu=0.2, vertex=vertex, max_iterations=60, **SMALL)
+    pm = MuParams(**{**p.__dict__, "mode": "moments"})
+    g = grid_for(p)
+    A, B, C = _state(g, 7)
+    d = iterate_mu_once(g, A, B, C, p)
+    m = iterate_mu_once(g, A, B, C, pm)
+    for x, y in zip(d, m):
+        assert np.array_equal(x.view(np.float64), y.view(np.float64))
+    if vertex == "bc":
+        return  # diverges under successive approximation (DESIGN.md)
+    sd, sm = solve_mu(p, g), solve_mu(pm, g)
+    assert (sd.iterations, sd.converged) == (sm.iterations, sm.converged)
+    for x, y in ((sd.A, sm.A), (sd.B, sm.B), (sd.C, sm.C)):
+        assert np.array_equal(x.view(np.float64), y.view(np.float64))
+
+
+def test_moments_mode_reuse_across_mu_and_failure():
+    """One sweeper serves several mu values from one moment table (config 4),
+    each bitwise equal to its direct solve; a non-finite state fails with the
+    reference's location."""
+    p = MuParams(vertex="bcb", max_iterations=80, mode="moments", **SMALL)
+    g = grid_for(p)
+    with MuSweeper(g, p) as sw:
+        for mu in (0.05, 0.3):
+            pm = MuParams(**{**p.__dict__, "mu": mu})
+            got = sw.solve(pm)
+            ref = solve_mu(MuParams(**{**pm.__dict__, "mode": "direct"}), g)
+            assert got.iterations == ref.iterations
+            assert np.array_equal(got.A.view(np.float64), ref.A.view(np.float64))
+        A, B, C = _state(g, 4)
+        A[3, 5] = np.nan
+        with pytest.raises(mu_oracle.MuNumericalFailure) as ref_exc:
+            mu_oracle.sweep(g, p, A, B, C)
+        with pytest.raises(NumericalFailureError) as got_exc:
+            sw.sweep(A, B, C)
+        assert (got_exc.value.row, got_exc.value.radial, got_exc.value.angular) == \
+            (ref_exc.value.row, ref_exc.value.radial, ref_exc.value.angular)

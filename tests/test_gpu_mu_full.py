@@ -59,3 +59,14 @@ def test_config3_row_sharding_bitwise(config3):
             parts[f].reshape(-1)[r::W] = x[f].reshape(-1)[r::W]
     for f in range(3):
         assert np.array_equal(parts[f].view(np.float64), full[f].view(np.float64))
+
+
+def test_config3_moments_mode_equals_direct():
+    p = MuParams()
+    g = grid_for(p)
+    with MuSweeper(g, p) as sw:
+        ref = sw.solve(p)
+        got = sw.solve(MuParams(**{**p.__dict__, "mode": "moments"}))
+    assert got.iterations == ref.iterations and got.converged
+    for x, y in ((got.A, ref.A), (got.B, ref.B), (got.C, ref.C)):
+        assert np.array_equal(x.view(np.float64), y.view(np.float64))
