@@ -22,6 +22,7 @@ from dataclasses import dataclass, field, replace
 import numpy as np
 
 from . import _native as nat
+from .errors import ParameterError
 from .mu_grid import MODES, VERTICES, MuGrid, MuParams, build_mu_grid, grid_for
 
 __all__ = ["MuIterationRecord", "MuSolution", "MuSweeper", "solve_mu", "iterate_mu_once", "solve_mu_batch",
@@ -53,6 +54,12 @@ class MuSolution:
         return self.B / self.A
 
 
+def _check_c_projection(grid: MuGrid, p: MuParams) -> None:
+    """C = z1 + P_C / p~4 needs p~4 = p4 + i mu != 0 at every external point."""
+    if p.mu == 0.0 and np.any(np.asarray(grid.p4_ext) == 0.0):
+        raise ParameterError("mu = 0 with an external p4 node at 0: the C projection divides by p4 + i mu")
+
+
 def _c_params(p: MuParams) -> nat.DseMuParams:
     return nat.DseMuParams(coeff=p.interaction_coeff, omega=p.omega, m0=p.m0, z1=p.z1, mu=p.mu, xi=p.xi,
                            relaxation=p.relaxation, max_iterations=int(p.max_iterations),
@@ -76,6 +83,7 @@ class MuSweeper:
 
     def __init__(self, grid: MuGrid, params: MuParams, device: int = 0, row_start: int = 0, row_stride: int = 1):
         params.validate()
+        _check_c_projection(grid, params)
         self.grid, self.params, self.device = grid, params, device
         lib = nat.load()
         self._keep = [np.ascontiguousarray(getattr(grid, n), dtype=np.float64) for n in
@@ -118,6 +126,7 @@ class MuSweeper:
     def solve(self, params: MuParams | None = None, a0=None, b0=None, c0=None, history: bool = True) -> MuSolution:
         p = self.params if params is None else params
         p.validate()
+        _check_c_projection(self.grid, p)
         shape = (self.grid.n_s, self.grid.n_4)
         A, B, C = _state(a0, shape, 1.0), _state(b0, shape, 0.3), _state(c0, shape, 1.0)
         hist = np.full((p.max_iterations + 1, 4), np.nan) if history else None

@@ -253,3 +253,14 @@ def test_moments_mode_reuse_across_mu_and_failure():
             sw.sweep(A, B, C)
         assert (got_exc.value.row, got_exc.value.radial, got_exc.value.angular) == \
             (ref_exc.value.row, ref_exc.value.radial, ref_exc.value.angular)
+
+
+@pytest.mark.parametrize("dims", [dict(n_s=2, n_4=2, m_s=2, m_4=2, m_ang=1), dict(n_s=3, n_4=5, m_s=7, m_4=4, m_ang=3)])
+def test_minimum_and_ragged_grids(dims):
+    p = MuParams(mu=0.15, **dims)
+    g = grid_for(p)
+    A, B, C = _state(g, 8)
+    got = iterate_mu_once(g, A, B, C, p)
+    ref = mu_oracle.sweep(g, p, A, B, C)
+    for x, r in zip(got, ref):
+        assert _cmp(x, r) < 1e-11

@@ -84,3 +84,26 @@ def test_mu0_bc1_restores_o4_symmetry():
     assert np.max(np.abs(A.imag)) == 0.0
     ir = slice(0, 6)
     assert np.max(np.abs(A[ir] - C[ir]) / np.abs(A[ir])) < 0.25
+
+
+def test_mu0_p4_zero_node_rejected_before_any_device_call():
+    from paper_2012_03667_b200.errors import ParameterError
+    from paper_2012_03667_b200.finite_mu import MuSweeper
+    p = MuParams(mu=0.0, n_s=4, n_4=5, m_s=6, m_4=6, m_ang=2)  # odd n_4: the middle midpoint is p4 = 0
+    g = grid_for(p)
+    assert np.any(g.p4_ext == 0.0)
+    with pytest.raises(ParameterError):
+        MuSweeper(g, p)
+
+
+def test_grid_rejects_bad_sizes():
+    from paper_2012_03667_b200.errors import ParameterError
+    for kw in (dict(n_s=1), dict(m_4=1), dict(m_ang=0)):
+        args = dict(n_s=4, n_4=4, m_s=4, m_4=4, m_ang=2)
+        args.update(kw)
+        with pytest.raises(ParameterError):
+            build_mu_grid(**args)
+    with pytest.raises(ParameterError):
+        MuParams(vertex="rainbow").validate()
+    with pytest.raises(ParameterError):
+        MuParams(mode="fast").validate()
