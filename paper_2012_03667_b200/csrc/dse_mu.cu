@@ -534,23 +534,50 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
             int top = 1;
             while (top < a.m_s) top <<= 1;
             const long long mbase = MOM ? __ldg(a.mo_base + r) : 0;
-            for (int f0 = 0; f0 < total; f0 += kThreads) {
-                const int f = min(f0 + tid, total - 1);
-                const int js = node_of(roff, a.m_s, top, f);
-                const int j4 = rlo[js] + (f - roff[js]);
-                __syncwarp();
-                double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-                if (MOM) {
-                    const double2* nb = a.NB + 4 * (size_t)(js * a.m_4 + j4);
-                    const double2 vn[4] = {nb[0], nb[1], nb[2], nb[3]};
-                    double mom[5];
+            if (MOM) {
+                // the moment stream is read once per iteration from HBM: the
+                // next pair's moments and node values are loaded before this
+                // pair is contracted (software pipelining over the row)
+                int f = min(tid, total - 1);
+                int js = node_of(roff, a.m_s, top, f), j4 = rlo[js] + (f - roff[js]);
+                double mom[5];
+                double2 vn[4];
+                if (total > 0) {
                     for (int q = 0; q < 5; ++q) mom[q] = __ldcs(a.mo_mom + q * a.mo_stride + mbase + f);
-                    pair_contract<V>(a, rc, js, j4, vn, mom, part);
-                } else {
-                    pair_contrib<V>(a, rc, js, j4, zw, tbl, part);
+                    const double2* nb = a.NB + 4 * (size_t)(js * a.m_4 + j4);
+                    for (int q = 0; q < 4; ++q) vn[q] = nb[q];
                 }
-                if (f0 + tid < total)
-                    for (int c = 0; c < 6; ++c) acc[c] += part[c];
+                for (int f0 = 0; f0 < total; f0 += kThreads) {
+                    const int fn = min(f0 + kThreads + tid, total - 1);
+                    const int jsn = node_of(roff, a.m_s, top, fn), j4n = rlo[jsn] + (fn - roff[jsn]);
+                    double momn[5];
+                    double2 vnn[4];
+                    if (f0 + kThreads < total) {
+                        for (int q = 0; q < 5; ++q) momn[q] = __ldcs(a.mo_mom + q * a.mo_stride + mbase + fn);
+                        const double2* nb = a.NB + 4 * (size_t)(jsn * a.m_4 + j4n);
+                        for (int q = 0; q < 4; ++q) vnn[q] = nb[q];
+                    }
+                    __syncwarp();
+                    double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                    pair_contract<V>(a, rc, js, j4, vn, mom, part);
+                    if (f0 + tid < total)
+                        for (int c = 0; c < 6; ++c) acc[c] += part[c];
+                    js = jsn;
+                    j4 = j4n;
+                    for (int q = 0; q < 5; ++q) mom[q] = momn[q];
+                    for (int q = 0; q < 4; ++q) vn[q] = vnn[q];
+                }
+            } else {
+                for (int f0 = 0; f0 < total; f0 += kThreads) {
+                    const int f = min(f0 + tid, total - 1);
+                    const int js = node_of(roff, a.m_s, top, f);
+                    const int j4 = rlo[js] + (f - roff[js]);
+                    __syncwarp();
+                    double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                    pair_contrib<V>(a, rc, js, j4, zw, tbl, part);
+                    if (f0 + tid < total)
+                        for (int c = 0; c < 6; ++c) acc[c] += part[c];
+                }
             }
             pairs += (tid == 0) ? total : 0;
             // fixed-order block reduction
