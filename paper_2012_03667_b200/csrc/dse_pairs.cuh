@@ -40,6 +40,9 @@ constexpr int kPairsThreads = 256;
 #define DSE_PAIRS_UNROLL 8  // measured at config 2: 2 -> 0.368, 4 -> 0.356, 8 -> 0.351 ms
 #endif
 constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
+// (requesting the next ticket while an item computes ran 0.353 vs 0.341 ms:
+// a busy warp then holds an item idle warps could run, the tail grows; angle
+// chunks C = 2 / 4 at config 2 ran 0.362 / 0.410 ms: per-item overhead)
 // (two accumulator sets for even/odd angles ran 0.344 vs 0.339 ms: the loop
 // is FP64-pipe bound, not add-chain bound)
 // (an 11-bit exp table with a degree-3 polynomial ran 0.333 ms but put a
