@@ -40,6 +40,9 @@ constexpr int kPairsThreads = 256;
 #define DSE_PAIRS_UNROLL 8  // measured at config 2: 2 -> 0.368, 4 -> 0.356, 8 -> 0.351 ms
 #endif
 constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
+// (sharing one exp between the symmetric angles z, -z -- exp(-kappa(-z)/w2)
+// = exp(-2 psum/w2) / exp(-kappa(z)/w2) -- ran 0.338 vs 0.342 ms and moved
+// one golden sweep past 1e-12: rejected)
 // (requesting the next ticket while an item computes ran 0.353 vs 0.341 ms:
 // a busy warp then holds an item idle warps could run, the tail grows; angle
 // chunks C = 2 / 4 at config 2 ran 0.362 / 0.410 ms: per-item overhead)
