@@ -499,8 +499,8 @@ def interp_bench(p, nat, torch, dev, hbm):
     return res
 
 
-# ncu SASS mix of mu_solve_kernel<bcb> (profiles/r01/SUMMARY.md): 2*DFMA + DMUL + DADD per evaluated point
-MU_FLOP_PER_POINT = 44.1
+# ncu SASS mix of mu_solve_kernel<bcb> (profiles/r01/mu_sweep.md): 2*DFMA + DMUL + DADD per evaluated point
+MU_FLOP_PER_POINT = 45.3
 
 
 def _mu_cpu_rows(args):
