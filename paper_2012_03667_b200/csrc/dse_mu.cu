@@ -59,6 +59,7 @@ struct MuArgs {
     int n_s, n_4, m_s, m_4, K;
     int row_start, row_stride, n_rows;  // owned external points: row_start + r*row_stride
     double coeff, w2, exp_c1, skip_k2, mu, z1, m0z1, xi, relax;
+    double dq_eps2;
     double2* X;            // [2][3][n_ext]
     double2* NB;           // [m_int][4]: A_q, B_q, C_q, 1/den
     double* bmax;          // [gridDim][3]
@@ -191,7 +192,9 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
     const double kts = Q2 - P2;
     // q~^2 - p~^2 = k.t (complex), real part as (Q2 - P2) + k4 (q4 + p4)
     const cplx kt = C(fma(k4, q4r + rc.p4r, kts), 2.0 * a.mu * k4);
-    const cplx rkt = rcp(kt);
+    // experiment hook (DSE_MU_DQ_EPS2, default 0 = the exact quotient):
+    // Tikhonov-regularised 1/(q~^2 - p~^2) = conj(d) / (|d|^2 + eps^2)
+    const cplx rkt = a.dq_eps2 > 0.0 ? (1.0 / fma(kt.x, kt.x, fma(kt.y, kt.y, a.dq_eps2))) * C(kt.x, -kt.y) : rcp(kt);
     const cplx sA = 0.5 * (rc.Ap + Aq), sC = 0.5 * (rc.Cp + Cq);
     const cplx dA = (Aq - rc.Ap) * rkt, dC = (Cq - rc.Cp) * rkt, dB = (Bq - rc.Bp) * rkt;
     const cplx tau0 = 2.0 * sA + sC;
@@ -771,6 +774,7 @@ mu::MuArgs mu_make_args(dse_mu_sweeper* s, const dse_mu_params& p, int it_begin,
     a.evaluated = count ? s->d_eval : nullptr;
     a.it_begin = it_begin; a.it_end = it_end; a.sweep_only = sweep_only ? 1 : 0;
     a.vertex = (int)p.vertex;
+    a.dq_eps2 = getenv("DSE_MU_DQ_EPS2") ? atof(getenv("DSE_MU_DQ_EPS2")) : 0.0;
     a.mo_rlo = s->d_mo_rlo; a.mo_roff = s->d_mo_roff; a.mo_base = s->d_mo_base; a.mo_mom = s->d_mo_mom;
     a.mo_stride = s->mo_total > 0 ? s->mo_total : 0;
     return a;
