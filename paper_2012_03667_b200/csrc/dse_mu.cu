@@ -524,6 +524,13 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
                     roff[js] = __ldg(a.mo_roff + (size_t)r * (a.m_s + 1) + js);
                 __syncthreads();
                 total = roff[a.m_s];
+            } else if (!all && a.mo_rlo) {
+                // the precomputed windows of this row (geometry + omega only)
+                for (int js = tid; js < a.m_s; js += kThreads) rlo[js] = __ldg(a.mo_rlo + (size_t)r * a.m_s + js);
+                for (int js = tid; js <= a.m_s; js += kThreads)
+                    roff[js] = __ldg(a.mo_roff + (size_t)r * (a.m_s + 1) + js);
+                __syncthreads();
+                total = roff[a.m_s];
             } else {
                 using Scan = cub::BlockScan<int, kThreads>;
                 __shared__ typename Scan::TempStorage scan_tmp;
@@ -743,6 +750,8 @@ struct dse_mu_sweeper {
     double* d_mo_mom = nullptr;
     long long mo_total = -1;
     bool mo_mode = false;  // the current call runs the moments kernel
+    double win_omega = -1.0;  // omega the windows were built for
+    long long win_pairs = 0;
 };
 
 namespace {
@@ -794,9 +803,16 @@ const void* mu_kernel_ptr(int v, bool mom = false) {
 // Moments mode: the windows and the five angular moments of every evaluated
 // pair of the owned rows, once per sweeper (they depend on the grid and
 // omega only, so every mu of a config-4 sweep reuses them).
-int mu_build_moments(dse_mu_sweeper* s, const dse_mu_params& p, dse_err* err) {
-    if (s->mo_total >= 0) return DSE_OK;
+// The exact-zero windows of every owned row (geometry + omega only) and the
+// rows' pair offsets into the moment table; used by both modes.
+int mu_build_windows(dse_mu_sweeper* s, const dse_mu_params& p, dse_err* err) {
+    if (s->win_omega == p.omega && s->d_mo_rlo) return DSE_OK;
     const size_t R = (size_t)s->n_rows, ms = (size_t)s->m_s;
+    if (s->d_mo_rlo) {  // a different omega: new windows, and the moments go stale
+        for (void* q : {(void*)s->d_mo_rlo, (void*)s->d_mo_roff, (void*)s->d_mo_base, (void*)s->d_mo_mom}) cudaFree(q);
+        s->d_mo_rlo = nullptr; s->d_mo_roff = nullptr; s->d_mo_base = nullptr; s->d_mo_mom = nullptr;
+        s->mo_total = -1;
+    }
     CUDA_TRY(cudaMalloc(&s->d_mo_rlo, R * ms * sizeof(int)));
     CUDA_TRY(cudaMalloc(&s->d_mo_roff, R * (ms + 1) * sizeof(int)));
     CUDA_TRY(cudaMalloc(&s->d_mo_base, R * sizeof(long long)));
@@ -822,6 +838,22 @@ int mu_build_moments(dse_mu_sweeper* s, const dse_mu_params& p, dse_err* err) {
         sum += tot[r];
     }
     CUDA_TRY(cudaMemcpyAsync(s->d_mo_base, base.data(), R * sizeof(long long), cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    s->win_pairs = sum;
+    s->win_omega = p.omega;
+    return DSE_OK;
+}
+
+int mu_build_moments(dse_mu_sweeper* s, const dse_mu_params& p, dse_err* err) {
+    int rc = mu_build_windows(s, p, err);
+    if (rc) return rc;
+    if (s->mo_total >= 0) return DSE_OK;
+    const size_t R = (size_t)s->n_rows, ms = (size_t)s->m_s;
+    (void)ms;
+    const long long sum = s->win_pairs;
+    mu::MuArgs a = mu_make_args(s, p, 0, 0, false, true, false);
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
     size_t free_b = 0, total_b = 0;
     CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
     if ((size_t)std::max(sum, 1ll) * 5 * sizeof(double) > free_b)
@@ -846,7 +878,7 @@ int mu_build_moments(dse_mu_sweeper* s, const dse_mu_params& p, dse_err* err) {
 // select the kernel family of this call; build the moment table on first use
 int mu_prepare(dse_mu_sweeper* s, const dse_mu_params& p, dse_err* err) {
     s->mo_mode = p.mode == DSE_MU_MODE_MOMENTS;
-    return s->mo_mode ? mu_build_moments(s, p, err) : DSE_OK;
+    return s->mo_mode ? mu_build_moments(s, p, err) : mu_build_windows(s, p, err);
 }
 
 int mu_launch(dse_mu_sweeper* s, const mu::MuArgs& a, bool reset, dse_err* err) {
