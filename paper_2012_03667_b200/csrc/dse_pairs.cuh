@@ -43,6 +43,8 @@ constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
 // (sharing one exp between the symmetric angles z, -z -- exp(-kappa(-z)/w2)
 // = exp(-2 psum/w2) / exp(-kappa(z)/w2) -- ran 0.338 vs 0.342 ms and moved
 // one golden sweep past 1e-12: rejected)
+// (an int2 (row, group) item table instead of one int and a division ran
+// 0.350 vs 0.342 ms)
 // (requesting the next ticket while an item computes ran 0.353 vs 0.341 ms:
 // a busy warp then holds an item idle warps could run, the tail grows; angle
 // chunks C = 2 / 4 at config 2 ran 0.362 / 0.410 ms: per-item overhead)
