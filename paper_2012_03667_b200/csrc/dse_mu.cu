@@ -560,6 +560,7 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
                 for (int f0 = 0; f0 < total; f0 += kThreads) {
                     const int fn = min(f0 + kThreads + tid, total - 1);
                     const int jsn = node_of(roff, a.m_s, top, fn), j4n = rlo[jsn] + (fn - roff[jsn]);
+                    DCHECK(jsn >= 0 && jsn < a.m_s && j4n >= 0 && j4n < a.m_4 && mbase + fn < a.mo_stride, 23);
                     double momn[5];
                     double2 vnn[4];
                     if (f0 + kThreads < total) {

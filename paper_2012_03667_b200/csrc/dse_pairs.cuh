@@ -120,6 +120,8 @@ __global__ void __launch_bounds__(kPairsThreads, DSE_PAIRS_MINB) dse_pairs_kerne
             const double a_p = __ldcg(Ac + i), b_p = __ldcg(Bc + i);
             const int2 win = __ldg(a.pr_win + r);
             const int j = 32 * g + lane;
+            DCHECK(r >= 0 && r < a.n_mrows && g >= 0 && g < G && c >= 0 && c < C && k0 >= 0 && k1 <= a.K, 20);
+            DCHECK(i >= 0 && i < a.N && win.x >= 0 && win.y <= a.M, 21);
             const bool all = any_bad || !isfinite(a_p) || !isfinite(b_p);
             const bool active = j < a.M && (all || (j >= win.x && j < win.y));
             double sa = 0.0, sb = 0.0;

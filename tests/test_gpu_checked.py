@@ -1,7 +1,8 @@
 """GPU: the bounds-checked build (compute-sanitizer is closed on this pool)
 runs every kernel path -- sweeps, solves (static and dynamic schedules, both
 arithmetics, split rows), batched solves, row_rhs, both interpolation modes,
-the reduction hook and the failure path -- with zero index violations."""
+the reduction hook and the failure path, the pairs arithmetic and the
+finite-mu kernels (direct and moments mode) -- with zero index violations."""
 import os
 import subprocess
 import sys
