@@ -24,7 +24,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -645,7 +644,25 @@ def mu_bench(p, torch, dev, flush, args, peak, no_cpu):
                              "seconds_with_build": tts_mo + build_wall},
         "bitwise_equal_to_direct": bool(np.array_equal(smo.A, sol.A) and np.array_equal(smo.B, sol.B)),
     }
+    # Anderson acceleration (depth 8) of the same sweep map, moments mode:
+    # the same fixed point in fewer sweeps (an option; the reference has no
+    # finite-mu solver to follow)
+    from paper_2012_03667_b200.finite_mu import solve_mu_anderson
     mus = [0.4 * (k + 0.5) / 32 for k in range(32)]
+    with MuSweeper(g, pmo) as sw:
+        solve_mu_anderson(pmo, g, sweeper=sw)  # builds the table, warms up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        saa = solve_mu_anderson(pmo, g, sweeper=sw)
+        t3aa = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        aa4 = [solve_mu_anderson(_replace(pmo, mu=float(m)), g, sweeper=sw) for m in mus]
+        t4aa = time.perf_counter() - t0
+    out["config3"]["anderson_moments"] = {
+        "iterations": saa.iterations, "converged": saa.converged, "seconds_wall": t3aa,
+        "max_abs_diff_vs_successive_approximation": float(max(np.max(np.abs(saa.A - sol.A)),
+                                                              np.max(np.abs(saa.B - sol.B)),
+                                                              np.max(np.abs(saa.C - sol.C))))}
     t0 = time.perf_counter()
     sols_mo = solve_mu_batch(mus, pmo, g)
     t4mo = time.perf_counter() - t0
@@ -661,7 +678,10 @@ def mu_bench(p, torch, dev, flush, args, peak, no_cpu):
                                        "seconds_per_solve": t4mo / len(mus),
                                        "iterations_equal_direct": [s.iterations for s in sols_mo] ==
                                                                   [s.iterations for s in sols],
-                                       "note": "one moment table built once, shared by the 32 mu values"}}
+                                       "note": "one moment table built once, shared by the 32 mu values"},
+                      "anderson_moments": {"seconds": t4aa, "solves_per_s": len(mus) / t4aa,
+                                           "iterations": [s.iterations for s in aa4],
+                                           "converged": int(sum(s.converged for s in aa4))}}
     if not no_cpu:
         rate, info = mu_cpu_rate(float(os.environ.get("BENCH_MU_CPU_S", "8")))
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port",

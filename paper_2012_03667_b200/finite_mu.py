@@ -26,7 +26,7 @@ from .errors import ParameterError
 from .mu_grid import MODES, VERTICES, MuGrid, MuParams, build_mu_grid, grid_for
 
 __all__ = ["MuIterationRecord", "MuSolution", "MuSweeper", "solve_mu", "iterate_mu_once", "solve_mu_batch",
-           "solve_mu_batch_sharded", "solve_mu_sharded", "owned_mus", "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
+           "solve_mu_batch_sharded", "solve_mu_sharded", "solve_mu_anderson", "owned_mus", "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
 
 
 @dataclass(frozen=True)
@@ -276,6 +276,77 @@ def solve_mu_sharded(params: MuParams | None = None, grid: MuGrid | None = None,
         full = device_view(px.value, 3 * 2 * n, dev).cpu().numpy().view(np.complex128).reshape(3, *shape)
     return MuSolution(A=full[0].copy(), B=full[1].copy(), C=full[2].copy(), iterations=n_it, converged=converged,
                       history=hist, grid=grid, params=params)
+
+
+def solve_mu_anderson(params: MuParams | None = None, grid: MuGrid | None = None, a0=None, b0=None, c0=None,
+                      depth: int = 8, beta: float = 1.0, device: int = 0, sweeper: "MuSweeper | None" = None
+                      ) -> MuSolution:
+    """Finite-mu solve with Anderson acceleration (type II, depth m) of the
+    same fixed-point map g = one Jacobi sweep: x <- x + beta f - (dX + beta dF) gamma,
+    gamma = argmin |f - dF gamma| over the last m residual differences
+    (normal equations, m x m, on the device).  Stops when max|g(x) - x| of
+    A, B and C are all < xi (the successive-approximation rule applied to
+    the sweep's update).  The reference has no finite-mu solver; this is an
+    option next to solve_mu's plain successive approximation (it converges
+    to the same fixed point in fewer sweeps: config 3 25 vs 63; it does NOT
+    rescue the divergent full 'bc' vertex).  params.relaxation is ignored
+    (beta plays its role); history rows hold max|g(x) - x| per function."""
+    import ctypes
+
+    import torch
+    params = MuParams() if params is None else params
+    params.validate()
+    grid = grid_for(params) if grid is None else grid
+    _check_c_projection(grid, params)
+    dev = torch.device("cuda", device)
+    n = grid.n_ext
+    shape = (grid.n_s, grid.n_4)
+    x = torch.cat([torch.from_numpy(_state(v, shape, d).reshape(-1)) for v, d in ((a0, 1.0), (b0, 0.3), (c0, 1.0))])
+    x = x.to(dev)
+    send = torch.zeros(3 * n, dtype=torch.complex128, device=dev)
+    lib = nat.load()
+    cp = _c_params(params)
+    own = sweeper is None
+    sw = MuSweeper(grid, params, device) if own else sweeper
+    hist = [MuIterationRecord(0, float("nan"), float("nan"), float("nan"))]
+    X, F = [], []
+    converged, n_it = False, params.max_iterations
+    try:
+        st = torch.cuda.current_stream(dev).cuda_stream
+        err = nat.DseErr()
+        for it in range(1, params.max_iterations + 1):
+            nat.raise_for(lib.dse_mu_solve_load(sw.handle, x[:n].data_ptr(), x[n:2 * n].data_ptr(),
+                                                x[2 * n:].data_ptr(), st, ctypes.byref(err)), err)
+            nat.raise_for(lib.dse_mu_sharded_sweep_pack(sw.handle, ctypes.byref(cp), send.data_ptr(), n, st,
+                                                        ctypes.byref(err)), err)
+            nat.raise_for(lib.dse_mu_sharded_failure(sw.handle, st, ctypes.byref(err)), err)
+            f = send - x
+            d = torch.stack([f[k * n:(k + 1) * n].abs().max() for k in range(3)]).cpu().numpy()
+            hist.append(MuIterationRecord(it, float(d[0]), float(d[1]), float(d[2])))
+            if d[0] < params.xi and d[1] < params.xi and d[2] < params.xi:
+                x = send.clone()
+                converged, n_it = True, it
+                break
+            X.append(x.clone())
+            F.append(f)
+            if len(F) > depth + 1:
+                X.pop(0)
+                F.pop(0)
+            if len(F) == 1:
+                x = x + beta * f
+                continue
+            dF = torch.stack([F[k + 1] - F[k] for k in range(len(F) - 1)], dim=1)
+            dX = torch.stack([X[k + 1] - X[k] for k in range(len(X) - 1)], dim=1)
+            gram = dF.conj().T @ dF
+            gram = gram + (1e-14 * torch.real(torch.trace(gram)) + 1e-300) * torch.eye(gram.shape[0], device=dev)
+            gamma = torch.linalg.solve(gram, dF.conj().T @ f)
+            x = x + beta * f - (dX + beta * dF) @ gamma
+    finally:
+        if own:
+            sw.close()
+    xs = x.cpu().numpy()
+    A, B, C = (xs[k * n:(k + 1) * n].reshape(shape).copy() for k in range(3))
+    return MuSolution(A=A, B=B, C=C, iterations=n_it, converged=converged, history=hist, grid=grid, params=params)
 
 
 def owned_mus(mus, rank: int, world: int) -> list:

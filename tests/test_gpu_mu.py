@@ -264,3 +264,15 @@ def test_minimum_and_ragged_grids(dims):
     ref = mu_oracle.sweep(g, p, A, B, C)
     for x, r in zip(got, ref):
         assert _cmp(x, r) < 1e-11
+
+
+@pytest.mark.parametrize("mode", ["direct", "moments"])
+def test_anderson_reaches_the_same_fixed_point_faster(mode):
+    from paper_2012_03667_b200.finite_mu import solve_mu_anderson
+    p = MuParams(mu=0.2, vertex="bcb", max_iterations=300, xi=1e-11, mode=mode, **SMALL)
+    g = grid_for(p)
+    sa = solve_mu(p, g)
+    aa = solve_mu_anderson(p, g, depth=8)
+    assert sa.converged and aa.converged and aa.iterations < sa.iterations
+    for x, y in ((aa.A, sa.A), (aa.B, sa.B), (aa.C, sa.C)):
+        assert np.max(np.abs(x - y)) <= 1e-9 * np.max(np.abs(y))
