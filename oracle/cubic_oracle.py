@@ -12,8 +12,12 @@ import numpy as np
 
 
 def brackets(x, q):
-    """_bracket_search semantics (interpolation.py:47-68) = searchsorted(right) - 1, clamped."""
-    return np.clip(np.searchsorted(x, q, side="right") - 1, -1, x.size - 1)
+    """_bracket_search semantics (interpolation.py:47-68): searchsorted(right) - 1,
+    clamped to [-1, n-1]; a NaN query fails both range tests and every
+    bisection compare, so the search ends at 0."""
+    q = np.asarray(q, np.float64)
+    i = np.clip(np.searchsorted(x, q, side="right") - 1, -1, x.size - 1)
+    return np.where(np.isnan(q), 0, i)
 
 
 def interp_cubic(x, v, coef, q):

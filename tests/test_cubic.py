@@ -34,6 +34,9 @@ def test_oracle_clamps_and_brackets():
     q = np.array([x[0] / 2, x[0], x[3], x[-1], 2 * x[-1]])
     val, idx = cubic_oracle.interp_cubic(x, v, cf, q)
     assert list(idx) == [-1, 0, 3, 15, 15]
+    # the reference's _bracket_search on NaN ends at 0 (interpolation.py:47-68)
+    nv, ni = cubic_oracle.interp_cubic(x, v, cf, np.array([np.nan]))
+    assert ni[0] == 0 and np.isnan(nv[0])
     assert val[0] == v[0] and val[1] == v[0] and val[2] == v[3] and val[3] == v[-1] and val[4] == v[-1]
 
 
@@ -43,12 +46,13 @@ def test_gpu_cubic_bitwise(mode):
     x, v = _table()
     rng = np.random.default_rng(0)
     q = np.exp(rng.uniform(np.log(1e-4), np.log(1e4), 1 << 18))
-    q = np.concatenate([q, x, [x[0] / 3, 1e5, x[-1], np.nextafter(x[-1], 0), np.nextafter(x[0], 1)]])
+    q = np.concatenate([q, x, [x[0] / 3, 1e5, x[-1], np.nextafter(x[-1], 0), np.nextafter(x[0], 1),
+                               np.nan, np.inf, -np.inf, 0.0]])
     cf = natural_cubic_coefficients(x, v)
     got, gidx = interp_cubic_batch(x, v, q, mode=mode, with_index=True)
     ref, ridx = cubic_oracle.interp_cubic(x, v, cf, q)
     assert np.array_equal(gidx, ridx)
-    assert np.array_equal(got, ref)
+    assert np.array_equal(got, ref, equal_nan=True)
 
 
 @pytest.mark.gpu
