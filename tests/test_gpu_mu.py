@@ -76,10 +76,12 @@ def test_sweep_row_sharding_and_grid_size_bitwise():
     try:
         with MuSweeper(g, p) as sw:
             few = sw.sweep(A, B, C)
+            few_mo = sw.sweep(A, B, C, MuParams(**{**p.__dict__, "mode": "moments"}))
     finally:
         del os.environ["DSE_MU_BLOCKS"]
     for f in range(3):
         assert np.array_equal(few[f].view(np.float64), full[f].view(np.float64))
+        assert np.array_equal(few_mo[f].view(np.float64), full[f].view(np.float64))
 
 
 @pytest.mark.parametrize("vertex", ["bcb", "bc1"])
