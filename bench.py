@@ -498,6 +498,21 @@ def interp_bench(p, nat, torch, dev, hbm):
     t0 = time.perf_counter()
     interp_cubic_batch(x, v, q, mode="direct")
     res["cubic_e2e_host_arrays_queries_per_s"] = n / (time.perf_counter() - t0)
+    # CPU baseline: the reference's interp_search_many restated in C
+    # (oracle/), all host threads, on a 2^22-query sample
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle
+        th = oracle.max_threads()
+        qs = q[: 1 << 22]
+        t0 = time.perf_counter()
+        oracle.interp_search_many(x, v, qs, threads=th)
+        dt = time.perf_counter() - t0
+        res["cpu_baseline"] = {"value": qs.size / dt, "unit": "queries/s", "cores": th, "kind": "port",
+                               "sample": f"{qs.size} of the 2^26 queries, binary search (interpolation.py:100-113) "
+                                         f"in C, oracle/dse_oracle.c"}
+    except Exception as exc:  # noqa: BLE001 -- a missing oracle build must not sink the GPU numbers
+        res["cpu_baseline"] = {"unavailable": str(exc)[:120]}
     return res
 
 
