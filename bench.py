@@ -520,36 +520,28 @@ def interp_bench(p, nat, torch, dev, hbm):
 MU_FLOP_PER_POINT = 45.3
 
 
-def _mu_cpu_rows(args):
+def mu_cpu_rate(budget_s: float):
+    """The finite-mu CPU oracle restated in C (oracle/mu_oracle_c.c, OpenMP
+    over external points, all host threads) on a row sample of config 3.
+    There is no reference CPU path for finite mu: this is
+    the restatement, kind "port"."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import mu_oracle
     from paper_2012_03667_b200.mu_grid import MuParams, grid_for
     p = MuParams()
     g = grid_for(p)
     shape = (g.n_s, g.n_4)
     A, B, C = np.ones(shape, complex), np.full(shape, 0.3 + 0j), np.ones(shape, complex)
-    Aq, Bq, Cq = (mu_oracle.interp2d(g, X) for X in (A, B, C))
+    cores = os.cpu_count() or 1
+    probe = np.arange(cores) * 131 % g.n_ext
     t0 = time.perf_counter()
-    for i in args:
-        mu_oracle.sweep_row(g, p, int(i), A, B, C, Aq, Bq, Cq)
-    return time.perf_counter() - t0
-
-
-def mu_cpu_rate(budget_s: float):
-    """The finite-mu CPU oracle (numpy, oracle/mu_oracle.py) on a row sample
-    of config 3, one process per host core.  There is no reference CPU path
-    for finite mu: this is the restatement, kind "port"."""
-    import multiprocessing as mp
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    cores = min(os.cpu_count() or 1, 32)
-    t1 = _mu_cpu_rows([8192])
-    per_core = max(1, int(budget_s / max(t1, 1e-3)))
-    rows = np.arange(cores * per_core) * 131 % (128 * 128)
-    chunks = [rows[c::cores].tolist() for c in range(cores)]
+    mu_oracle.sweep_rows_c(g, p, A, B, C, probe, threads=cores)
+    per_row = (time.perf_counter() - t0) / probe.size
+    rows = np.arange(max(cores, int(budget_s / max(per_row, 1e-6)))) * 131 % g.n_ext
     t0 = time.perf_counter()
-    with mp.get_context("fork").Pool(cores) as pool:
-        pool.map(_mu_cpu_rows, chunks)
+    mu_oracle.sweep_rows_c(g, p, A, B, C, rows, threads=cores)
     dt = time.perf_counter() - t0
-    pts = rows.size * 128 * 128 * 32
+    pts = rows.size * g.m_int * g.m_ang
     return pts / dt, {"rows": int(rows.size), "points": int(pts), "seconds": dt, "cores": cores}
 
 
@@ -700,8 +692,8 @@ def mu_bench(p, torch, dev, flush, args, peak, no_cpu):
     if not no_cpu:
         rate, info = mu_cpu_rate(float(os.environ.get("BENCH_MU_CPU_S", "8")))
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port",
-                               "sample": f"{info['rows']} config-3 rows x full 128x128x32 block, numpy oracle "
-                                         f"oracle/mu_oracle.py ({info['seconds']:.1f} s)"}
+                               "sample": f"{info['rows']} config-3 rows x full 128x128x32 block, C restatement "
+                                         f"oracle/mu_oracle_c.c ({info['seconds']:.1f} s)"}
     return out
 
 

@@ -37,7 +37,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["interp2d", "point_projections", "sweep_row", "sweep", "solve", "delta"]
+__all__ = ["interp2d", "point_projections", "sweep_row", "sweep", "solve", "delta", "sweep_rows_c"]
 
 
 def _lin(xi, xi1, vi, vi1, q):
@@ -235,3 +235,60 @@ def solve(grid, params, A0=None, B0=None, C0=None):
         if all(x < params.xi for x in d):
             return A, B, C, n, True, hist
     return A, B, C, params.max_iterations, False, hist
+
+
+_CLIB = None
+
+
+def _clib():
+    """liboracle_mu.so (mu_oracle_c.c, the same per-point formula in C with
+    OpenMP over points; built by oracle/Makefile)."""
+    global _CLIB
+    if _CLIB is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        path = os.path.join(here, "liboracle_mu.so")
+        src = os.path.join(here, "mu_oracle_c.c")
+        if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
+            subprocess.run(["make", "-s", "-C", here, "liboracle_mu.so"], check=True)
+        lib = ctypes.CDLL(path)
+        f64 = ctypes.POINTER(ctypes.c_double)
+        i64 = ctypes.c_int64
+        lib.mu_sweep_rows.restype = ctypes.c_int
+        lib.mu_sweep_rows.argtypes = [f64, f64, i64, i64, f64, f64, f64, i64, i64, f64, f64, i64,
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_double, ctypes.c_int, f64, f64, f64, f64, f64, f64,
+                                      ctypes.POINTER(ctypes.c_int64), i64, f64, ctypes.c_int]
+        _CLIB = lib
+    return _CLIB
+
+
+def sweep_rows_c(grid, params, A, B, C, rows, threads: int | None = None):
+    """(A', B', C') at the listed external points, C restatement (sequential
+    sums over (j_s, j_4, k) per point; np.sum's pairwise order in sweep_row
+    differs at the rounding level).  Returns complex array [len(rows), 3]."""
+    import ctypes
+    import os
+    lib = _clib()
+    shape = (grid.n_s, grid.n_4)
+    A, B, C = (np.ascontiguousarray(np.asarray(x, np.complex128).reshape(shape)) for x in (A, B, C))
+    Aq, Bq, Cq = (np.ascontiguousarray(interp2d(grid, X)) for X in (A, B, C))
+    rows = np.ascontiguousarray(np.asarray(rows, np.int64))
+    out = np.empty((rows.size, 3), np.complex128)
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+    keep = [np.ascontiguousarray(getattr(grid, n), dtype=np.float64) for n in
+            ("p_ext", "p4_ext", "q_int", "q4_int", "node_measure", "z_nodes", "z_weights")]
+    ptr = [k.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) for k in keep]
+    cv = lambda a: a.view(np.float64).ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+    vertex = ("bc", "bc1", "bcb").index(params.vertex)
+    bad = lib.mu_sweep_rows(ptr[0], ptr[1], grid.n_s, grid.n_4, ptr[2], ptr[3], ptr[4], grid.m_s, grid.m_4, ptr[5],
+                            ptr[6], grid.m_ang, params.interaction_coeff, params.omega, params.mu, params.z1,
+                            params.m0, vertex, cv(A), cv(B), cv(C), cv(Aq), cv(Bq), cv(Cq),
+                            rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), rows.size, cv(out),
+                            int(threads or os.cpu_count() or 1))
+    del f
+    if bad:
+        raise MuNumericalFailure(-1, -1, -1)
+    return out

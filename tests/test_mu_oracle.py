@@ -107,3 +107,20 @@ def test_grid_rejects_bad_sizes():
         MuParams(vertex="rainbow").validate()
     with pytest.raises(ParameterError):
         MuParams(mode="fast").validate()
+
+
+@pytest.mark.parametrize("vertex", ["bc", "bc1", "bcb"])
+def test_c_restatement_matches_numpy_oracle(vertex):
+    p = MuParams(mu=0.2, vertex=vertex, n_s=8, n_4=10, m_s=12, m_4=14, m_ang=6)
+    g = grid_for(p)
+    rng = np.random.default_rng(3)
+    shape = (g.n_s, g.n_4)
+    A = 1 + rng.random(shape) + 0.1j * rng.standard_normal(shape)
+    B = 0.2 + 0.3 * rng.random(shape) + 0.05j * rng.standard_normal(shape)
+    C = 1 + rng.random(shape) + 0.1j * rng.standard_normal(shape)
+    rows = np.arange(g.n_ext)
+    got = mu_oracle.sweep_rows_c(g, p, A, B, C, rows, threads=2)
+    ref = mu_oracle.sweep(g, p, A, B, C)
+    for f in range(3):
+        r = ref[f].reshape(-1)
+        assert np.max(np.abs(got[:, f] - r)) <= 1e-12 * np.max(np.abs(r))
