@@ -654,8 +654,13 @@ def mu_bench(p, torch, dev, flush, args, peak, no_cpu):
     # Anderson acceleration (depth 8) of the same sweep map, moments mode:
     # the same fixed point in fewer sweeps (an option; the reference has no
     # finite-mu solver to follow)
-    from paper_2012_03667_b200.finite_mu import solve_mu_anderson
+    from paper_2012_03667_b200.finite_mu import solve_mu_anderson, solve_mu_batch_anderson
     mus = [0.4 * (k + 0.5) / 32 for k in range(32)]
+    solve_mu_batch_anderson(mus[:4], pmo, g)  # warm-up (kernels, allocations)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    bb = solve_mu_batch_anderson(mus, pmo, g, batch=4)
+    t4b = time.perf_counter() - t0
     with MuSweeper(g, pmo) as sw:
         solve_mu_anderson(pmo, g, sweeper=sw)  # builds the table, warms up
         torch.cuda.synchronize()
@@ -688,7 +693,13 @@ def mu_bench(p, torch, dev, flush, args, peak, no_cpu):
                                        "note": "one moment table built once, shared by the 32 mu values"},
                       "anderson_moments": {"seconds": t4aa, "solves_per_s": len(mus) / t4aa,
                                            "iterations": [s.iterations for s in aa4],
-                                           "converged": int(sum(s.converged for s in aa4))}}
+                                           "converged": int(sum(s.converged for s in aa4))},
+                      "batched_anderson_moments": {
+                          "seconds": t4b, "solves_per_s": len(mus) / t4b, "batch": 4,
+                          "iterations": [s.iterations for s in bb], "converged": int(sum(s.converged for s in bb)),
+                          "note": "groups of 4 mu values swept by one kernel (dse_mu_batch_sweep: the moment "
+                                  "table read once per pair for the group), batched Anderson algebra; includes "
+                                  "the moment-table build"}}
     if not no_cpu:
         rate, info = mu_cpu_rate(float(os.environ.get("BENCH_MU_CPU_S", "8")))
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port",

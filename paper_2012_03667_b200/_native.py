@@ -147,6 +147,9 @@ _PROTOS = [
                                                ctypes.POINTER(DseErr)]),
     ("dse_mu_sharded_failure", ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
     ("dse_mu_sweeper_state", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    ("dse_mu_batch_sweep", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DseMuParams), ctypes.c_int64,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, i64p,
+                                          ctypes.POINTER(DseErr)]),
     ("dse_mu_sweeper_stats", ctypes.c_int, [ctypes.c_void_p, i64p, i64p, i32p, i64p]),
     ("dse_launch_count", ctypes.c_int64, []),
 ]

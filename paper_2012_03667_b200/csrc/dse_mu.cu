@@ -139,6 +139,7 @@ __device__ void build_nodes(const MuArgs& a, const double2* __restrict__ Xin, in
 struct RowC {
     double P, P2, p4r;
     cplx p4t, Ap, Bp, Cp;
+    double mu, coeff;  // per solve (batched sweeps carry several)
 };
 
 // One (row, node) pair: angular moments, then the complex contraction.
@@ -186,12 +187,12 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
     const double S0 = mom[0], S1 = mom[1], T0 = mom[2], T1 = mom[3], T2 = mom[4];
     const double2 vA = vn[0], vB = vn[1], vC = vn[2], vR = vn[3];
     const cplx Aq = C(vA.x, vA.y), Bq = C(vB.x, vB.y), Cq = C(vC.x, vC.y);
-    const cplx q4t = C(q4r, a.mu);
-    const cplx t4 = C(q4r + rc.p4r, 2.0 * a.mu);
+    const cplx q4t = C(q4r, rc.mu);
+    const cplx t4 = C(q4r + rc.p4r, 2.0 * rc.mu);
     const double P2 = rc.P2;
     const double kts = Q2 - P2;
     // q~^2 - p~^2 = k.t (complex), real part as (Q2 - P2) + k4 (q4 + p4)
-    const cplx kt = C(fma(k4, q4r + rc.p4r, kts), 2.0 * a.mu * k4);
+    const cplx kt = C(fma(k4, q4r + rc.p4r, kts), 2.0 * rc.mu * k4);
     // experiment hook (DSE_MU_DQ_EPS2, default 0 = the exact quotient):
     // Tikhonov-regularised 1/(q~^2 - p~^2) = conj(d) / (|d|^2 + eps^2)
     const cplx rkt = a.dq_eps2 > 0.0 ? (1.0 / fma(kt.x, kt.x, fma(kt.y, kt.y, a.dq_eps2))) * C(kt.x, -kt.y) : rcp(kt);
@@ -259,7 +260,7 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
     const cplx FA = cfma(cA00, S0, cfma(cA01, S1, cfma(cA10, T0, cfma(cA11, T1, T2 * cA12))));
     const cplx FC = cfma(cC00, S0, cfma(cC01, S1, cfma(cC10, T0, T1 * cC11)));
     const cplx FB = cfma(cB00, S0, cfma(cB01, S1, cfma(cB10, T0, T1 * cB11)));
-    const double sc = a.coeff * (__ldg(a.meas_s + js) * __ldg(a.meas_4 + j4));
+    const double sc = rc.coeff * (__ldg(a.meas_s + js) * __ldg(a.meas_4 + j4));
     const cplx rd = sc * C(vR.x, vR.y);
     const cplx gA = FA * rd, gB = FB * rd, gC = FC * rd;
     acc[0] += gA.x; acc[1] += gA.y;
@@ -396,6 +397,8 @@ __device__ __forceinline__ RowC row_consts(const MuArgs& a, const double2* Xin, 
     rc.Ap = C(va.x, va.y);
     rc.Bp = C(vb.x, vb.y);
     rc.Cp = C(vc.x, vc.y);
+    rc.mu = a.mu;
+    rc.coeff = a.coeff;
     return rc;
 }
 
@@ -671,6 +674,121 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
     }
 }
 
+
+// ---- batched sweeps (BASELINE config 4): S independent solves on one grid,
+// one launch per sweep, in moments mode.  Every pair's five moments are read
+// once and contracted S times (each solve has its own state, node table, mu
+// and coefficient); the per-solve arithmetic and reduction order are those of
+// mu_solve_kernel<V, true>, so each solve's sweep is bitwise its standalone
+// moments-mode sweep.
+constexpr int kMuMaxBatch = 4;
+struct MuBatch {
+    const double2* Xin;   // [S][3][n_ext]
+    double2* Xout;        // [S][3][n_ext]
+    double2* NB;          // [S][m_int][4]
+    unsigned long long* err;  // [S] lowest failing row
+    int* nonfinite;       // [S]
+    double mu[kMuMaxBatch], coeff[kMuMaxBatch], z1[kMuMaxBatch], m0z1[kMuMaxBatch];
+};
+
+template <int V, int S>
+__global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_batch_kernel(MuArgs a, MuBatch b) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double smem[];
+    double* red = smem;                                            // kWarps * 6 * S
+    int* rlo = reinterpret_cast<int*>(red + kWarps * 6 * S);       // m_s
+    int* roff = rlo + a.m_s;                                       // m_s + 1
+    __shared__ RowC s_rc[S];
+    __shared__ unsigned s_row;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_ext = a.n_s * a.n_4, m_int = a.m_s * a.m_4;
+    // phase I: every solve's node table (its state, its mu)
+    for (int s = 0; s < S; ++s) {
+        MuArgs as = a;
+        as.mu = b.mu[s];
+        as.NB = b.NB + (size_t)s * 4 * m_int;
+        build_nodes(as, b.Xin + (size_t)s * 3 * n_ext, b.nonfinite + s);
+    }
+    grid.sync();
+    int top = 1;
+    while (top < a.m_s) top <<= 1;
+    for (;;) {
+        if (tid == 0) s_row = atomicAdd(a.ctr, 1u);
+        __syncthreads();
+        const unsigned r = s_row;
+        __syncthreads();
+        if (r >= (unsigned)a.n_rows) break;
+        const int i = a.row_start + (int)r * a.row_stride;
+        if (tid < S) {
+            MuArgs as = a;
+            as.mu = b.mu[tid];
+            as.coeff = b.coeff[tid];
+            s_rc[tid] = row_consts(as, b.Xin + (size_t)tid * 3 * n_ext, n_ext, i);
+        }
+        for (int js = tid; js < a.m_s; js += kThreads) rlo[js] = __ldg(a.mo_rlo + (size_t)r * a.m_s + js);
+        for (int js = tid; js <= a.m_s; js += kThreads) roff[js] = __ldg(a.mo_roff + (size_t)r * (a.m_s + 1) + js);
+        __syncthreads();
+        const int total = roff[a.m_s];
+        const long long mbase = __ldg(a.mo_base + r);
+        double acc[S][6];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) acc[s][c] = 0.0;
+        for (int f0 = 0; f0 < total; f0 += kThreads) {
+            const int f = min(f0 + tid, total - 1);
+            const int js = node_of(roff, a.m_s, top, f);
+            const int j4 = rlo[js] + (f - roff[js]);
+            DCHECK(total == 0 || (js >= 0 && js < a.m_s && j4 >= 0 && j4 < a.m_4), 24);
+            double mom[5];
+            for (int q = 0; q < 5; ++q) mom[q] = __ldcs(a.mo_mom + q * a.mo_stride + mbase + f);
+            __syncwarp();
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const double2* nb = b.NB + (size_t)s * 4 * m_int + 4 * (size_t)(js * a.m_4 + j4);
+                const double2 vn[4] = {nb[0], nb[1], nb[2], nb[3]};
+                double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                pair_contract<V>(a, s_rc[s], js, j4, vn, mom, part);
+                if (f0 + tid < total)
+                    for (int c = 0; c < 6; ++c) acc[s][c] += part[c];
+            }
+        }
+        // fixed-order block reduction per solve (mu_solve_kernel's)
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                double v = acc[s][c];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) red[(warp * S + s) * 6 + c] = v;
+            }
+        __syncthreads();
+        if (tid < S) {
+            const int s = tid;
+            const RowC& rc = s_rc[s];
+            double sum[6];
+            for (int c = 0; c < 6; ++c) {
+                double v = red[s * 6 + c];
+                for (int w = 1; w < kWarps; ++w) v += red[(w * S + s) * 6 + c];
+                sum[c] = v;
+            }
+            const double2 An = make_double2(b.z1[s] + sum[0] / rc.P2, sum[1] / rc.P2);
+            const double2 Bn = make_double2(b.m0z1[s] + sum[2], sum[3]);
+            const cplx cn = C(sum[4], sum[5]) * rcp(rc.p4t);
+            const double2 Cn = make_double2(b.z1[s] + cn.x, cn.y);
+            const bool fin = isfinite(An.x) && isfinite(An.y) && isfinite(Bn.x) && isfinite(Bn.y) &&
+                             isfinite(Cn.x) && isfinite(Cn.y);
+            if (!fin || b.nonfinite[s]) atomicMin(b.err + s, (unsigned long long)(b.nonfinite[s] ? a.row_start : i));
+            double2* Xo = b.Xout + (size_t)s * 3 * n_ext;
+            Xo[i] = An;
+            Xo[n_ext + i] = Bn;
+            Xo[2 * n_ext + i] = Cn;
+        }
+        __syncthreads();
+    }
+}
+
 // Failure location: first non-finite point (j, k) in row-major order of the
 // failing row, evaluated with the same pair form.  One thread per node.
 template <int V>
@@ -692,6 +810,8 @@ __global__ void __launch_bounds__(kThreads) mu_locate_kernel(MuArgs a, int i, in
     rc.Ap = C(Xin[i].x, Xin[i].y);
     rc.Bp = C(Xin[n_ext + i].x, Xin[n_ext + i].y);
     rc.Cp = C(Xin[2 * n_ext + i].x, Xin[2 * n_ext + i].y);
+    rc.mu = a.mu;
+    rc.coeff = a.coeff;
     // per point: run the pair form with a single-angle weight table
     double2 zw1[1];
     MuArgs b = a;
@@ -752,6 +872,10 @@ struct dse_mu_sweeper {
     long long mo_total = -1;
     bool mo_mode = false;  // the current call runs the moments kernel
     double win_omega = -1.0;  // omega the windows were built for
+    double2* d_bNB = nullptr;  // batched sweeps: [S][m_int][4] node tables
+    unsigned long long* d_berr = nullptr;
+    int* d_bnf = nullptr;
+    int bblocks[2] = {0, 0};   // cooperative grid of the batch kernels (S = 2, 4)
     long long win_pairs = 0;
 };
 
@@ -1034,7 +1158,8 @@ int dse_mu_sweeper_destroy(dse_mu_sweeper* s) {
                     (void*)s->d_ms, (void*)s->d_m4, (void*)s->d_z, (void*)s->d_wz, (void*)s->d_etbl,
                     (void*)s->d_brk_s, (void*)s->d_brk_4, (void*)s->d_X, (void*)s->d_NB, (void*)s->d_bmax,
                     (void*)s->d_ctr, (void*)s->d_err, (void*)s->d_status, (void*)s->d_eval, (void*)s->d_hist, (void*)s->d_nonfinite,
-                    (void*)s->d_mo_rlo, (void*)s->d_mo_roff, (void*)s->d_mo_base, (void*)s->d_mo_mom})
+                    (void*)s->d_mo_rlo, (void*)s->d_mo_roff, (void*)s->d_mo_base, (void*)s->d_mo_mom,
+                    (void*)s->d_bNB, (void*)s->d_berr, (void*)s->d_bnf})
         if (p) cudaFree(p);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;
@@ -1248,6 +1373,81 @@ int dse_mu_sharded_failure(dse_mu_sweeper* s, uintptr_t stream, dse_err* err) {
 int dse_mu_sweeper_state(dse_mu_sweeper* s, double** dX) {
     if (!s || !dX) return DSE_EPARAM;
     *dX = (double*)s->d_X;  // [3][n_ext] complex: A, B, C
+    return DSE_OK;
+}
+
+int dse_mu_batch_sweep(dse_mu_sweeper* s, const dse_mu_params* params, int64_t S, const double* dX_in,
+                       double* dX_out, uintptr_t stream, int64_t* failed_row, dse_err* err) {
+    ok(err);
+    if (!s || !params || !dX_in || !dX_out || !failed_row || (S != 2 && S != 4))
+        return fail(err, DSE_EPARAM, "bad argument (S must be 2 or 4)");
+    for (int64_t q = 0; q < S; ++q) {
+        int rc = mu_check_params(params + q, err);
+        if (rc) return rc;
+        if (params[q].omega != params[0].omega || params[q].vertex != params[0].vertex)
+            return fail(err, DSE_EPARAM, "batched solves share omega and the vertex");
+    }
+    if (s->row_start != 0 || s->row_stride != 1) return fail(err, DSE_EPARAM, "batched sweeps need every row");
+    CUDA_TRY(cudaSetDevice(s->device));
+    dse_mu_params p0 = params[0];
+    p0.mode = DSE_MU_MODE_MOMENTS;
+    int rc = mu_build_moments(s, p0, err);
+    if (rc) return rc;
+    const size_t m_int = (size_t)s->m_s * s->m_4, ne = (size_t)s->n_s * s->n_4;
+    if (!s->d_bNB) {
+        CUDA_TRY(cudaMalloc(&s->d_bNB, sizeof(double2) * 4 * m_int * mu::kMuMaxBatch));
+        CUDA_TRY(cudaMalloc(&s->d_berr, sizeof(unsigned long long) * mu::kMuMaxBatch));
+        CUDA_TRY(cudaMalloc(&s->d_bnf, sizeof(int) * mu::kMuMaxBatch));
+    }
+    const int v = (int)p0.vertex, si = S == 2 ? 0 : 1;
+    auto kp = [&](int vv, int64_t ss) -> const void* {
+        if (ss == 2) return vv == DSE_MU_VERTEX_BC1 ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC1, 2>
+                          : vv == DSE_MU_VERTEX_BCB ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BCB, 2>
+                                                    : (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC, 2>;
+        return vv == DSE_MU_VERTEX_BC1 ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC1, 4>
+             : vv == DSE_MU_VERTEX_BCB ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BCB, 4>
+                                       : (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC, 4>;
+    };
+    const size_t smem = (size_t)mu::kWarps * 6 * S * sizeof(double) + (2 * (size_t)s->m_s + 2) * sizeof(int);
+    if (!s->bblocks[si]) {
+        int per_sm = 1 << 30, sms = 0;
+        for (int vv : {DSE_MU_VERTEX_BC, DSE_MU_VERTEX_BC1, DSE_MU_VERTEX_BCB}) {
+            CUDA_TRY(cudaFuncSetAttribute(kp(vv, S), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int n = 0;
+            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kp(vv, S), mu::kThreads, smem));
+            per_sm = std::min(per_sm, n);
+        }
+        CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+        if (per_sm < 1) return fail(err, DSE_EENV, "batched kernel does not fit on an SM");
+        s->bblocks[si] = per_sm * sms;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    mu::mu_reset_kernel<<<1, 32, 0, st>>>(s->d_ctr, s->d_err, s->d_status, s->d_nonfinite);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaMemsetAsync(s->d_berr, 0xff, sizeof(unsigned long long) * S, st));
+    CUDA_TRY(cudaMemsetAsync(s->d_bnf, 0, sizeof(int) * S, st));
+    mu::MuArgs a = mu_make_args(s, p0, 0, 1, false, true, false);
+    mu::MuBatch b{};
+    b.Xin = (const double2*)dX_in;
+    b.Xout = (double2*)dX_out;
+    b.NB = s->d_bNB;
+    b.err = s->d_berr;
+    b.nonfinite = s->d_bnf;
+    for (int64_t q = 0; q < S; ++q) {
+        b.mu[q] = params[q].mu;
+        b.coeff[q] = params[q].coeff;
+        b.z1[q] = params[q].z1;
+        b.m0z1[q] = params[q].m0 * params[q].z1;
+    }
+    void* args[] = {&a, &b};
+    CUDA_TRY(cudaLaunchCooperativeKernel(kp(v, S), dim3(s->bblocks[si]), dim3(mu::kThreads), args, smem, st));
+    g_launches.fetch_add(1);
+    unsigned long long er[mu::kMuMaxBatch];
+    CUDA_TRY(cudaMemcpyAsync(er, s->d_berr, sizeof(unsigned long long) * S, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    (void)ne;
+    for (int64_t q = 0; q < S; ++q) failed_row[q] = er[q] == ~0ull ? -1 : (int64_t)er[q];
     return DSE_OK;
 }
 

@@ -26,7 +26,7 @@ from .errors import ParameterError
 from .mu_grid import MODES, VERTICES, MuGrid, MuParams, build_mu_grid, grid_for
 
 __all__ = ["MuIterationRecord", "MuSolution", "MuSweeper", "solve_mu", "iterate_mu_once", "solve_mu_batch",
-           "solve_mu_batch_sharded", "solve_mu_sharded", "solve_mu_anderson", "owned_mus", "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
+           "solve_mu_batch_sharded", "solve_mu_sharded", "solve_mu_anderson", "solve_mu_batch_anderson", "owned_mus", "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
 
 
 @dataclass(frozen=True)
@@ -175,6 +175,18 @@ class MuSweeper:
         """Enqueue the next n_iterations of the on-device loop (no stop test, no sync)."""
         err = nat.DseErr()
         nat.raise_for(self._lib.dse_mu_solve_resume(self._h, n_iterations, stream, ctypes.byref(err)), err)
+
+    def batch_sweep(self, x_in, x_out, params_list, stream: int = 0):
+        """One sweep of S = 2 or 4 independent states (dse_mu_batch_sweep,
+        moments mode): x_in, x_out device complex128 tensors [S, 3, n_ext];
+        returns the per-solve lowest failing row (-1 = fine)."""
+        S = len(params_list)
+        cps = (nat.DseMuParams * S)(*[_c_params(p) for p in params_list])
+        failed = (ctypes.c_int64 * S)()
+        err = nat.DseErr()
+        nat.raise_for(self._lib.dse_mu_batch_sweep(self._h, cps, S, x_in.data_ptr(), x_out.data_ptr(), stream,
+                                                   failed, ctypes.byref(err)), err)
+        return list(failed)
 
     def stats(self) -> dict:
         nom, ev, sm = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
@@ -347,6 +359,81 @@ def solve_mu_anderson(params: MuParams | None = None, grid: MuGrid | None = None
     xs = x.cpu().numpy()
     A, B, C = (xs[k * n:(k + 1) * n].reshape(shape).copy() for k in range(3))
     return MuSolution(A=A, B=B, C=C, iterations=n_it, converged=converged, history=hist, grid=grid, params=params)
+
+
+def solve_mu_batch_anderson(mus, params: MuParams | None = None, grid: MuGrid | None = None, depth: int = 8,
+                            beta: float = 1.0, batch: int = 4, device: int = 0) -> list:
+    """BASELINE config 4 on one GPU: the mu values in groups of `batch`
+    (2 or 4) swept together by dse_mu_batch_sweep (one moment table for all,
+    read once per pair per group sweep), each solve Anderson-accelerated like
+    solve_mu_anderson (same update, same stop rule, its own history)."""
+    import torch
+    params = MuParams() if params is None else params
+    params = replace(params, mode="moments")
+    params.validate()
+    grid = grid_for(params) if grid is None else grid
+    if batch not in (2, 4):
+        raise ParameterError("batch must be 2 or 4")
+    dev = torch.device("cuda", device)
+    n = grid.n_ext
+    shape = (grid.n_s, grid.n_4)
+    init = torch.cat([torch.full((n,), v, dtype=torch.complex128) for v in (1.0, 0.3, 1.0)]).to(dev)
+    out_all = []
+    with MuSweeper(grid, params, device) as sw:
+        mus = list(mus)
+        for g0 in range(0, len(mus), batch):
+            group = mus[g0:g0 + batch]
+            S = 4 if len(group) > 2 else 2
+            plist = [replace(params, mu=float(m)) for m in group]
+            plist += [plist[-1]] * (S - len(plist))  # pad with a repeat (its result is dropped)
+            for p_ in plist:
+                _check_c_projection(grid, p_)
+            x = init.repeat(S, 1).contiguous()
+            gx = torch.empty_like(x)
+            Xh, Fh = [], []  # histories as [S, 3n] tensors: the AA algebra is batched over the group
+            hist = [[MuIterationRecord(0, float("nan"), float("nan"), float("nan"))] for _ in range(S)]
+            res = [None] * S
+            its = [params.max_iterations] * S
+            for it in range(1, params.max_iterations + 1):
+                failed = sw.batch_sweep(x, gx, plist, torch.cuda.current_stream(dev).cuda_stream)
+                for s in range(S):
+                    if res[s] is None and failed[s] >= 0:
+                        from .errors import NumericalFailureError
+                        raise NumericalFailureError(f"non-finite integrand in batched finite-mu sweep, mu="
+                                                    f"{plist[s].mu}, row={failed[s]}", row=failed[s], iteration=it)
+                fx = gx - x
+                d = fx.view(S, 3, n).abs().amax(dim=2).cpu().numpy()
+                for s in range(S):
+                    if res[s] is not None:
+                        continue
+                    hist[s].append(MuIterationRecord(it, float(d[s, 0]), float(d[s, 1]), float(d[s, 2])))
+                    if d[s, 0] < params.xi and d[s, 1] < params.xi and d[s, 2] < params.xi:
+                        res[s] = gx[s].clone()
+                        its[s] = it
+                if all(r is not None for r in res):
+                    break
+                Xh.append(x)
+                Fh.append(fx)
+                if len(Fh) > depth + 1:
+                    Xh.pop(0)
+                    Fh.pop(0)
+                if len(Fh) == 1:
+                    x = x + beta * fx
+                    continue
+                # per solve (batched): gamma = argmin |f - dF gamma|, x <- x + beta f - (dX + beta dF) gamma
+                dF = torch.stack([Fh[k + 1] - Fh[k] for k in range(len(Fh) - 1)], dim=2)  # [S, 3n, L]
+                dX = torch.stack([Xh[k + 1] - Xh[k] for k in range(len(Xh) - 1)], dim=2)
+                gram = dF.conj().transpose(1, 2) @ dF                                     # [S, L, L]
+                tr = torch.real(torch.diagonal(gram, dim1=1, dim2=2).sum(dim=1))
+                gram = gram + (1e-14 * tr + 1e-300)[:, None, None] * torch.eye(gram.shape[1], device=dev)
+                gamma = torch.linalg.solve(gram, (dF.conj().transpose(1, 2) @ fx[:, :, None]))   # [S, L, 1]
+                x = x + beta * fx - ((dX + beta * dF) @ gamma)[:, :, 0]
+            for s in range(len(group)):
+                xs = (res[s] if res[s] is not None else x[s]).cpu().numpy()
+                A, B, C = (xs[k * n:(k + 1) * n].reshape(shape).copy() for k in range(3))
+                out_all.append(MuSolution(A=A, B=B, C=C, iterations=its[s], converged=res[s] is not None,
+                                          history=hist[s], grid=grid, params=plist[s]))
+    return out_all
 
 
 def owned_mus(mus, rank: int, world: int) -> list:

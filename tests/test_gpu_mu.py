@@ -278,3 +278,38 @@ def test_anderson_reaches_the_same_fixed_point_faster(mode):
     assert sa.converged and aa.converged and aa.iterations < sa.iterations
     for x, y in ((aa.A, sa.A), (aa.B, sa.B), (aa.C, sa.C)):
         assert np.max(np.abs(x - y)) <= 1e-9 * np.max(np.abs(y))
+
+
+@pytest.mark.parametrize("S", [2, 4])
+def test_batched_sweep_bitwise_equals_single(S):
+    """dse_mu_batch_sweep: each solve's sweep is bitwise its standalone
+    moments-mode sweep (own mu, D and state; shared moment table)."""
+    import torch
+    p = MuParams(vertex="bcb", mode="moments", **SMALL)
+    g = grid_for(p)
+    plist = [MuParams(**{**p.__dict__, "mu": 0.05 + 0.1 * s, "D": 0.5 + 0.02 * s}) for s in range(S)]
+    states = [_state(g, 20 + s) for s in range(S)]
+    dev = torch.device("cuda", 0)
+    x = torch.stack([torch.from_numpy(np.concatenate([v.reshape(-1) for v in st])) for st in states]).to(dev)
+    y = torch.empty_like(x)
+    with MuSweeper(g, p) as sw:
+        failed = sw.batch_sweep(x, y, plist)
+        assert failed == [-1] * S
+        for s in range(S):
+            ref = sw.sweep(*states[s], plist[s])
+            got = y[s].cpu().numpy()
+            for f in range(3):
+                part = got[f * g.n_ext:(f + 1) * g.n_ext].reshape(g.n_s, g.n_4)
+                assert np.array_equal(part.view(np.float64), ref[f].view(np.float64))
+
+
+def test_batched_anderson_matches_single_anderson():
+    from paper_2012_03667_b200.finite_mu import solve_mu_anderson, solve_mu_batch_anderson
+    p = MuParams(vertex="bcb", mode="moments", max_iterations=200, **SMALL)
+    g = grid_for(p)
+    mus = [0.05, 0.15, 0.25]
+    batch = solve_mu_batch_anderson(mus, p, g, batch=4)
+    for m, sol in zip(mus, batch):
+        one = solve_mu_anderson(MuParams(**{**p.__dict__, "mu": m}), g)
+        assert sol.converged and sol.iterations == one.iterations
+        assert np.max(np.abs(sol.A - one.A)) <= 1e-12 * np.max(np.abs(one.A))
