@@ -43,6 +43,11 @@ for dims in (dict(n_s=10, n_4=12, m_s=14, m_4=16, m_ang=6), dict(n_s=2, n_4=2, m
     mp = MuParams(max_iterations=3, **dims)
     with MuSweeper(grid_for(mp), mp, row_start=0, row_stride=3) as sw:
         sw.sweep(np.ones((mp.n_s, mp.n_4)), np.full((mp.n_s, mp.n_4), 0.3), np.ones((mp.n_s, mp.n_4)))
+# batched finite-mu sweeps (moments mode), S = 2 and 4
+from paper_2012_03667_b200.finite_mu import solve_mu_batch_anderson  # noqa: E402
+for bsz in (2, 4):
+    mp = MuParams(max_iterations=3, mode="moments", n_s=10, n_4=12, m_s=14, m_4=16, m_ang=6)
+    solve_mu_batch_anderson([0.1, 0.2, 0.3], mp, grid_for(mp), batch=bsz)
 flags = ctypes.c_uint32(0)
 assert _native.load().dse_debug_check_flags(ctypes.byref(flags)) == 0
 print("CHECK_FLAGS", flags.value)
