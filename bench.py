@@ -250,6 +250,8 @@ def run_ours(args):
                 "host_buffers": "pinned (numpy views of pinned torch tensors)"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": _load_profile_traffic(),
+                     "bound_note": "the FP64 vector pipe: neither HBM (0.25 MB per launch) nor tensor cores "
+                                   "(the integrand is not a dense contraction, north_star)",
                      "flop_per_point": FLOP_PER_POINT, "points": "evaluated (exact-zero pairs skipped)",
                      "peak_source": "measured: dse_fp64_peak DFMA probe on this GPU (MEASURED_PEAKS.json has no fp64)"},
         "cpu_baseline": cpu,
