@@ -327,7 +327,8 @@ def time_to_solution(p, torch, dev, arith):
         "substitute_256x256x256_relax0.5": dict(N=256, m_rad=256, m_ang=256, xi=1e-10, max_iterations=2000,
                                                 relaxation=0.5),
     }
-    ariths = [arith] + ([p.Arithmetic.FAST] if arith is not p.Arithmetic.FAST else [])
+    # the bench arithmetic, the fast one, and the exact one (the reference's own variant names map to it)
+    ariths = [arith] + [a for a in (p.Arithmetic.FAST, p.Arithmetic.EXACT) if a is not arith]
     for name, kw in cases.items():
         prm = p.ModelParams(**kw)
         g = p.build_grid(prm.N, prm.m_rad, prm.m_ang, prm.p2_min, prm.p2_max)
