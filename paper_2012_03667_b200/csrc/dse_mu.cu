@@ -50,6 +50,18 @@ __device__ __forceinline__ cplx rcp(cplx a) {
     const double d = 1.0 / fma(ax, ax, ay * ay);
     return C(ax * d * is, -ay * d * is);
 }
+// 1/a for the per-pair quotient 1/(q~^2 - p~^2): a power-of-two scale from
+// the exponent bits (exact) and the Newton reciprocal instead of two IEEE
+// divides (MUFU + two Newton steps, <= 1 ulp); a zero or non-finite a gives a
+// non-finite result as rcp() does
+__device__ __forceinline__ cplx rcp_pair(cplx a) {
+    const double s = fmax(fabs(a.x), fabs(a.y));
+    const int e = (__double2hiint(s) >> 20) & 0x7ff;
+    const double is = __hiloint2double((2046 - e) << 20, 0);  // 2^-(e - 1023)
+    const double ax = a.x * is, ay = a.y * is;
+    const double d = dse::rcp_nr(fma(ax, ax, ay * ay));
+    return C(ax * d * is, -ay * d * is);
+}
 // a*x + y for complex a, real x, complex y
 __device__ __forceinline__ cplx cfma(cplx a, double x, cplx y) { return C(fma(a.x, x, y.x), fma(a.y, x, y.y)); }
 
@@ -179,7 +191,14 @@ __device__ __forceinline__ void pair_moments(const MuArgs& a, const RowC& rc, in
 
 // The complex contraction of a pair's moments; acc[0..5] += (A, B, C) * meas
 // * coeff / den (before the row's division by |p|^2 and p~4).
-template <int V>
+// LATE_B: apply the B channel's common factor Bq after the contraction
+// (fewer operations: config 3 direct 5.16 -> 5.13 ms, batched S=4 5.11 ->
+// 5.01 ms).  With the trimmed zero terms and rcp_pair, 5.28 -> 5.13 ms direct,
+// 2.06 -> 1.83 ms moments, 5.59 -> 5.01 ms batched (S=4).
+#ifndef DSE_MU_LATE_B
+#define DSE_MU_LATE_B 1
+#endif
+template <int V, bool LATE_B = DSE_MU_LATE_B>
 __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, int js, int j4, const double2* vn,
                                               const double mom[5], double acc[6]) {
     const double Q2 = __ldg(a.Q2 + js), q4r = __ldg(a.q4 + j4);
@@ -195,7 +214,7 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
     const cplx kt = C(fma(k4, q4r + rc.p4r, kts), 2.0 * rc.mu * k4);
     // experiment hook (DSE_MU_DQ_EPS2, default 0 = the exact quotient):
     // Tikhonov-regularised 1/(q~^2 - p~^2) = conj(d) / (|d|^2 + eps^2)
-    const cplx rkt = a.dq_eps2 > 0.0 ? (1.0 / fma(kt.x, kt.x, fma(kt.y, kt.y, a.dq_eps2))) * C(kt.x, -kt.y) : rcp(kt);
+    const cplx rkt = a.dq_eps2 > 0.0 ? (1.0 / fma(kt.x, kt.x, fma(kt.y, kt.y, a.dq_eps2))) * C(kt.x, -kt.y) : rcp_pair(kt);
     const cplx sA = 0.5 * (rc.Ap + Aq), sC = 0.5 * (rc.Cp + Cq);
     const cplx dA = (Aq - rc.Ap) * rkt, dC = (Cq - rc.Cp) * rkt, dB = (Bq - rc.Bp) * rkt;
     const cplx tau0 = 2.0 * sA + sC;
@@ -220,7 +239,7 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
     // A channel (e = p_vec): F_A = cA00 + cA01 r + K (cA10 + cA11 r + cA12 r^2)
     const cplx lam0 = akQp + sA * akQ;
     const cplx cA00 = fac ? (-0.5 * P2) * (nu0 + dA * eta0) : zero;
-    cplx cA01 = Aq * tau0 - 2.0 * sAAq;
+    cplx cA01 = Aq * sC;  // Aq tau0 - 2 sA Aq
     cplx cA10 = (-P2) * lam0;
     cplx cA11 = lam0 + (2.0 * P2) * sAAq + Aq * tau1;
     if (fac) {
@@ -243,12 +262,23 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
         cC10 = cC10 - 0.5 * (Cq_q4t * psi - kt * (k4 * nu0 + dCt4 * akQ));
         cC11 = cC11 - 0.5 * (kt * (dCt4 * Aq - k4 * nu1));
     }
-    // B channel: F_B = cB00 + cB01 r + K (cB10 + cB11 r)
-    cplx cB00 = Bq * tau0, cB01 = zero, cB10 = Bq * tau1, cB11 = zero;
+    // B channel: F_B = cB00 + cB01 r + K (cB10 + cB11 r); without Delta_B
+    // every coefficient carries the factor Bq, which is applied once (with
+    // the scale) after the moments are contracted
+    constexpr bool late_b = LATE_B && !fdb;
+    cplx cB00, cB01 = zero, cB10, cB11 = zero;
     if (fb) {
-        cB00 = cB00 + Bq * (0.5 * delta0);
-        cB01 = Bq * dA;
-        cB10 = cB10 - Bq * (0.5 * psi);
+        cB00 = tau0 + 0.5 * delta0;
+        cB01 = dA;
+        cB10 = tau1 - 0.5 * psi;
+    } else {
+        cB00 = tau0;
+        cB10 = tau1;
+    }
+    if (!late_b) {
+        cB00 = Bq * cB00;
+        cB01 = Bq * cB01;
+        cB10 = Bq * cB10;
     }
     if (fdb) {
         cB00 = cB00 - dB * eta0;
@@ -257,12 +287,18 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
         cB11 = -1.0 * (dB * (kt * Aq));
     }
     // contract with the moments, scale by meas * coeff / den
-    const cplx FA = cfma(cA00, S0, cfma(cA01, S1, cfma(cA10, T0, cfma(cA11, T1, T2 * cA12))));
-    const cplx FC = cfma(cC00, S0, cfma(cC01, S1, cfma(cC10, T0, T1 * cC11)));
-    const cplx FB = cfma(cB00, S0, cfma(cB01, S1, cfma(cB10, T0, T1 * cB11)));
+    // (terms whose coefficient is identically zero for this vertex are not
+    // formed: 0 * moment would only matter for a non-finite moment, and a
+    // non-finite moment already makes the other terms non-finite)
+    const cplx FA0 = cfma(cA01, S1, cfma(cA10, T0, cfma(cA11, T1, T2 * cA12)));
+    const cplx FA = fac ? cfma(cA00, S0, FA0) : FA0;
+    const cplx FC0 = cfma(cC10, T0, T1 * cC11);
+    const cplx FC = cfma(cC00, S0, fac ? cfma(cC01, S1, FC0) : FC0);
+    const cplx FB0 = fdb ? cfma(cB10, T0, T1 * cB11) : T0 * cB10;
+    const cplx FB = cfma(cB00, S0, fb ? cfma(cB01, S1, FB0) : FB0);
     const double sc = rc.coeff * (__ldg(a.meas_s + js) * __ldg(a.meas_4 + j4));
     const cplx rd = sc * C(vR.x, vR.y);
-    const cplx gA = FA * rd, gB = FB * rd, gC = FC * rd;
+    const cplx gA = FA * rd, gB = FB * (late_b ? Bq * rd : rd), gC = FC * rd;
     acc[0] += gA.x; acc[1] += gA.y;
     acc[2] += gB.x; acc[3] += gB.y;
     acc[4] += gC.x; acc[5] += gC.y;
@@ -468,8 +504,17 @@ __global__ void __launch_bounds__(kThreads) mu_moments_build_kernel(MuArgs a) {
     }
 }
 
+#ifndef DSE_MU_MOM_PF_NB
+// moments mode: prefetch the next pair's node values with its moments (1) or
+// load them at use (0): config 3, 1.97 (early B) / 2.32 (late B) vs 1.83 ms
+#define DSE_MU_MOM_PF_NB 0
+#endif
+constexpr bool kMomPfNB = DSE_MU_MOM_PF_NB;
+#ifndef DSE_MU_MOM_MINB
+#define DSE_MU_MOM_MINB DSE_MU_MINB
+#endif
 template <int V, bool MOM>
-__global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs a) {
+__global__ void __launch_bounds__(kThreads, MOM ? DSE_MU_MOM_MINB : DSE_MU_MINB) mu_solve_kernel(MuArgs a) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) double smem[];
     double* etbl = smem;                                           // 2^bits
@@ -549,16 +594,18 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
             const long long mbase = MOM ? __ldg(a.mo_base + r) : 0;
             if (MOM) {
                 // the moment stream is read once per iteration from HBM: the
-                // next pair's moments and node values are loaded before this
-                // pair is contracted (software pipelining over the row)
+                // next pair's moments are loaded before this pair is
+                // contracted (software pipelining over the row)
                 int f = min(tid, total - 1);
                 int js = node_of(roff, a.m_s, top, f), j4 = rlo[js] + (f - roff[js]);
                 double mom[5];
                 double2 vn[4];
                 if (total > 0) {
                     for (int q = 0; q < 5; ++q) mom[q] = __ldcs(a.mo_mom + q * a.mo_stride + mbase + f);
-                    const double2* nb = a.NB + 4 * (size_t)(js * a.m_4 + j4);
-                    for (int q = 0; q < 4; ++q) vn[q] = nb[q];
+                    if (kMomPfNB) {
+                        const double2* nb = a.NB + 4 * (size_t)(js * a.m_4 + j4);
+                        for (int q = 0; q < 4; ++q) vn[q] = nb[q];
+                    }
                 }
                 for (int f0 = 0; f0 < total; f0 += kThreads) {
                     const int fn = min(f0 + kThreads + tid, total - 1);
@@ -568,8 +615,14 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
                     double2 vnn[4];
                     if (f0 + kThreads < total) {
                         for (int q = 0; q < 5; ++q) momn[q] = __ldcs(a.mo_mom + q * a.mo_stride + mbase + fn);
-                        const double2* nb = a.NB + 4 * (size_t)(jsn * a.m_4 + j4n);
-                        for (int q = 0; q < 4; ++q) vnn[q] = nb[q];
+                        if (kMomPfNB) {
+                            const double2* nb = a.NB + 4 * (size_t)(jsn * a.m_4 + j4n);
+                            for (int q = 0; q < 4; ++q) vnn[q] = nb[q];
+                        }
+                    }
+                    if (!kMomPfNB) {  // node values (L1/L2-resident) loaded at use
+                        const double2* nb = a.NB + 4 * (size_t)(js * a.m_4 + j4);
+                        for (int q = 0; q < 4; ++q) vn[q] = nb[q];
                     }
                     __syncwarp();
                     double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -579,7 +632,8 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_solve_kernel(MuArgs 
                     js = jsn;
                     j4 = j4n;
                     for (int q = 0; q < 5; ++q) mom[q] = momn[q];
-                    for (int q = 0; q < 4; ++q) vn[q] = vnn[q];
+                    if (kMomPfNB)
+                        for (int q = 0; q < 4; ++q) vn[q] = vnn[q];
                 }
             } else {
                 for (int f0 = 0; f0 < total; f0 += kThreads) {
