@@ -148,6 +148,20 @@ __device__ void build_nodes(const MuArgs& a, const double2* __restrict__ Xin, in
     }
 }
 
+// cp.async staging (moments mode): each thread copies its own next pair's
+// moments and node values into its own shared-memory slot and reads only that
+// slot, so a per-thread wait_group orders it (no block barrier)
+constexpr int kStageDoubles = 14;  // 4 node double2 (8) + 5 moments + 1 pad: 112 B, 16-B aligned
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dse::smem_addr(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dse::smem_addr(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 struct RowC {
     double P, P2, p4r;
     cplx p4t, Ap, Bp, Cp;
@@ -510,6 +524,14 @@ __global__ void __launch_bounds__(kThreads) mu_moments_build_kernel(MuArgs a) {
 #define DSE_MU_MOM_PF_NB 0
 #endif
 constexpr bool kMomPfNB = DSE_MU_MOM_PF_NB;
+#ifndef DSE_MU_MOM_STAGE
+// moments mode: cp.async staging of the next pair into shared memory
+// (supersedes the register prefetch above; spills 88 -> 32 B).  Config 3:
+// 1.84 -> 1.79 ms with the node values L1-cached (.ca); bypassing L1 (.cg)
+// was slower, 2.04 ms -- the node values are reused from L1 across pairs
+#define DSE_MU_MOM_STAGE 1
+#endif
+constexpr bool kMomStage = DSE_MU_MOM_STAGE;
 #ifndef DSE_MU_MOM_MINB
 #define DSE_MU_MOM_MINB DSE_MU_MINB
 #endif
@@ -523,6 +545,9 @@ __global__ void __launch_bounds__(kThreads, MOM ? DSE_MU_MOM_MINB : DSE_MU_MINB)
     double* q4s = red + kWarps * 6;                                // m_4
     int* rlo = reinterpret_cast<int*>(q4s + a.m_4);                // m_s: first evaluated j4 per js
     int* roff = rlo + a.m_s;                                       // m_s + 1: flat offsets
+    // moments mode: 2 x kThreads staging slots, 16-B aligned after roff
+    double* mom_stage = reinterpret_cast<double*>(
+        (reinterpret_cast<uintptr_t>(roff + a.m_s + 1) + 15) & ~uintptr_t(15));
     __shared__ unsigned s_row;
     __shared__ int s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -592,7 +617,53 @@ __global__ void __launch_bounds__(kThreads, MOM ? DSE_MU_MOM_MINB : DSE_MU_MINB)
             int top = 1;
             while (top < a.m_s) top <<= 1;
             const long long mbase = MOM ? __ldg(a.mo_base + r) : 0;
-            if (MOM) {
+            if (MOM && kMomStage) {
+                // the next pair's node values and moments are copied into this
+                // thread's shared-memory slot (cp.async, double-buffered)
+                // while the current pair is contracted
+                double* const slot0 = mom_stage + (size_t)tid * kStageDoubles;
+                constexpr size_t kBufStride = (size_t)kThreads * kStageDoubles;
+                int js = 0, j4 = 0;
+                if (total > 0) {
+                    const int f = min(tid, total - 1);
+                    js = node_of(roff, a.m_s, top, f);
+                    j4 = rlo[js] + (f - roff[js]);
+                    const double2* nb = a.NB + 4 * (size_t)(js * a.m_4 + j4);
+                    for (int q = 0; q < 4; ++q) cp_async16(slot0 + 2 * q, nb + q);
+                    for (int q = 0; q < 5; ++q) cp_async8(slot0 + 8 + q, a.mo_mom + q * a.mo_stride + mbase + f);
+                    cp_async_commit();
+                }
+                int buf = 0;
+                for (int f0 = 0; f0 < total; f0 += kThreads) {
+                    int jsn = js, j4n = j4;
+                    if (f0 + kThreads < total) {
+                        const int fn = min(f0 + kThreads + tid, total - 1);
+                        jsn = node_of(roff, a.m_s, top, fn);
+                        j4n = rlo[jsn] + (fn - roff[jsn]);
+                        DCHECK(jsn >= 0 && jsn < a.m_s && j4n >= 0 && j4n < a.m_4 && mbase + fn < a.mo_stride, 23);
+                        double* sl = slot0 + (buf ^ 1) * kBufStride;
+                        const double2* nb = a.NB + 4 * (size_t)(jsn * a.m_4 + j4n);
+                        for (int q = 0; q < 4; ++q) cp_async16(sl + 2 * q, nb + q);
+                        for (int q = 0; q < 5; ++q) cp_async8(sl + 8 + q, a.mo_mom + q * a.mo_stride + mbase + fn);
+                        cp_async_commit();
+                        cp_async_wait<1>();
+                    } else {
+                        cp_async_wait<0>();
+                    }
+                    const double* sl = slot0 + buf * kBufStride;
+                    const double2* sv = reinterpret_cast<const double2*>(sl);
+                    const double2 vn[4] = {sv[0], sv[1], sv[2], sv[3]};
+                    const double mom[5] = {sl[8], sl[9], sl[10], sl[11], sl[12]};
+                    __syncwarp();
+                    double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                    pair_contract<V>(a, rc, js, j4, vn, mom, part);
+                    if (f0 + tid < total)
+                        for (int c = 0; c < 6; ++c) acc[c] += part[c];
+                    js = jsn;
+                    j4 = j4n;
+                    buf ^= 1;
+                }
+            } else if (MOM) {
                 // the moment stream is read once per iteration from HBM: the
                 // next pair's moments are loaded before this pair is
                 // contracted (software pipelining over the row)
@@ -915,7 +986,7 @@ struct dse_mu_sweeper {
     double* d_hist = nullptr;
     size_t hist_cap = 0;
     int blocks = 0;
-    size_t smem = 0;
+    size_t smem = 0, smem_mom = 0;
     long long it_next = 0;
     long long evaluated_pairs = -1;
     // moments mode tables (built on first use; geometry only, shared by every mu)
@@ -1069,8 +1140,9 @@ int mu_launch(dse_mu_sweeper* s, const mu::MuArgs& a, bool reset, dse_err* err) 
     }
     mu::MuArgs b = a;
     void* args[] = {&b};
-    CUDA_TRY(cudaLaunchCooperativeKernel(mu_kernel_ptr(a.vertex, a.mo_mom != nullptr && s->mo_mode), dim3(s->blocks), dim3(mu::kThreads), args,
-                                         s->smem, s->stream));
+    const bool mom = a.mo_mom != nullptr && s->mo_mode;
+    CUDA_TRY(cudaLaunchCooperativeKernel(mu_kernel_ptr(a.vertex, mom), dim3(s->blocks), dim3(mu::kThreads), args,
+                                         mom ? s->smem_mom : s->smem, s->stream));
     g_launches.fetch_add(1);
     return DSE_OK;
 }
@@ -1184,13 +1256,15 @@ int dse_mu_sweeper_create(const dse_mu_grid* g, const dse_mu_params* p, int devi
     MU_TRY(cudaMalloc(&s->d_eval, sizeof(long long)));
     s->smem = (size_t)((1 << dse::kExpTableBits) + 2 * s->K + mu::kWarps * 6 + s->m_4) * sizeof(double) +
               (size_t)(2 * s->m_s + 2) * sizeof(int);
+    s->smem_mom = mu::kMomStage ? ((s->smem + 15) & ~size_t(15)) + 2 * sizeof(double) * mu::kThreads * mu::kStageDoubles
+                                : s->smem;
     int per_sm = 1 << 30, sms = 0;
     for (int v : {DSE_MU_VERTEX_BC, DSE_MU_VERTEX_BC1, DSE_MU_VERTEX_BCB})
         for (bool mom : {false, true}) {
-            MU_TRY(cudaFuncSetAttribute(mu_kernel_ptr(v, mom), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)s->smem));
+            const size_t sz = mom ? s->smem_mom : s->smem;
+            MU_TRY(cudaFuncSetAttribute(mu_kernel_ptr(v, mom), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sz));
             int n = 0;
-            MU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mu_kernel_ptr(v, mom), mu::kThreads, s->smem));
+            MU_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mu_kernel_ptr(v, mom), mu::kThreads, sz));
             per_sm = std::min(per_sm, n);
         }
     MU_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
