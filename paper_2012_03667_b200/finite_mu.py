@@ -290,6 +290,38 @@ def solve_mu_sharded(params: MuParams | None = None, grid: MuGrid | None = None,
                       history=hist, grid=grid, params=params)
 
 
+def _aa_system(dF, f):
+    """Normal equations of one solve's Anderson step, gamma = argmin
+    |f - dF gamma|: the Gram matrix dF^H dF [L, L] and dF^H f [L], as
+    elementwise products reduced over the 3n axis (a fixed-shape reduction:
+    bandwidth-bound, where a complex GEMM with M = N = L, K = 3n ran at 0.6 ms
+    per call), flattened into one complex vector for a single host copy.
+    dF [3n, L], f [3n] complex.  A solve batched with others forms bitwise the
+    system it forms alone."""
+    cdF = dF.conj()
+    return ((cdF[:, :, None] * dF[:, None, :]).sum(dim=0).reshape(-1), (cdF * f[:, None]).sum(dim=0))
+
+
+def _aa_solve(gram: np.ndarray, rhs: np.ndarray) -> np.ndarray:
+    """The L x L regularised solve on the host (LAPACK, one small matrix per
+    solve: identical alone or stacked), gram [..., L, L], rhs [..., L]."""
+    L = gram.shape[-1]
+    tr = np.real(np.trace(gram, axis1=-2, axis2=-1))
+    reg = gram + (1e-14 * tr + 1e-300)[..., None, None] * np.eye(L)
+    return np.linalg.solve(reg, rhs[..., None])[..., 0]
+
+
+def _aa_combine(dX, dF, gamma, beta):
+    """(dX + beta dF) @ gamma as an explicit fixed-order sum over the L columns
+    (elementwise: identical for a solve alone and in a batch).  dX, dF
+    [..., 3n, L]; gamma [..., L]."""
+    acc = None
+    for k in range(dF.shape[-1]):
+        t = (dX[..., k] + beta * dF[..., k]) * gamma[..., k:k + 1]
+        acc = t if acc is None else acc + t
+    return acc
+
+
 def solve_mu_anderson(params: MuParams | None = None, grid: MuGrid | None = None, a0=None, b0=None, c0=None,
                       depth: int = 8, beta: float = 1.0, device: int = 0, sweeper: "MuSweeper | None" = None
                       ) -> MuSolution:
@@ -333,26 +365,31 @@ def solve_mu_anderson(params: MuParams | None = None, grid: MuGrid | None = None
                                                         ctypes.byref(err)), err)
             nat.raise_for(lib.dse_mu_sharded_failure(sw.handle, st, ctypes.byref(err)), err)
             f = send - x
-            d = torch.stack([f[k * n:(k + 1) * n].abs().max() for k in range(3)]).cpu().numpy()
+            dmax = f.view(3, n).abs().amax(dim=1)
+            # the Anderson system with this residual appended is formed before
+            # the stop test, so that the deltas and the system reach the host
+            # in one copy (one sync per sweep)
+            Xt, Ft = (X + [x.clone()])[-(depth + 1):], (F + [f])[-(depth + 1):]
+            if len(Ft) > 1:
+                dF = torch.stack([Ft[k + 1] - Ft[k] for k in range(len(Ft) - 1)], dim=1)
+                dX = torch.stack([Xt[k + 1] - Xt[k] for k in range(len(Xt) - 1)], dim=1)
+                g_, r_ = _aa_system(dF, f)
+                host = torch.cat([dmax.to(torch.complex128), g_, r_]).cpu().numpy()
+            else:
+                host = dmax.cpu().numpy()
+            d = np.real(host[:3])
             hist.append(MuIterationRecord(it, float(d[0]), float(d[1]), float(d[2])))
             if d[0] < params.xi and d[1] < params.xi and d[2] < params.xi:
                 x = send.clone()
                 converged, n_it = True, it
                 break
-            X.append(x.clone())
-            F.append(f)
-            if len(F) > depth + 1:
-                X.pop(0)
-                F.pop(0)
+            X, F = Xt, Ft
             if len(F) == 1:
                 x = x + beta * f
                 continue
-            dF = torch.stack([F[k + 1] - F[k] for k in range(len(F) - 1)], dim=1)
-            dX = torch.stack([X[k + 1] - X[k] for k in range(len(X) - 1)], dim=1)
-            gram = dF.conj().T @ dF
-            gram = gram + (1e-14 * torch.real(torch.trace(gram)) + 1e-300) * torch.eye(gram.shape[0], device=dev)
-            gamma = torch.linalg.solve(gram, dF.conj().T @ f)
-            x = x + beta * f - (dX + beta * dF) @ gamma
+            L = len(F) - 1
+            gamma = _aa_solve(host[3:3 + L * L].reshape(L, L), host[3 + L * L:])
+            x = x + beta * f - _aa_combine(dX, dF, torch.from_numpy(gamma).to(dev), beta)
     finally:
         if own:
             sw.close()
@@ -402,7 +439,20 @@ def solve_mu_batch_anderson(mus, params: MuParams | None = None, grid: MuGrid | 
                         raise NumericalFailureError(f"non-finite integrand in batched finite-mu sweep, mu="
                                                     f"{plist[s].mu}, row={failed[s]}", row=failed[s], iteration=it)
                 fx = gx - x
-                d = fx.view(S, 3, n).abs().amax(dim=2).cpu().numpy()
+                dmax = fx.view(S, 3, n).abs().amax(dim=2)
+                # the Anderson systems with this residual appended are formed
+                # before the stop test: deltas and systems in one host copy
+                Xt, Ft = (Xh + [x])[-(depth + 1):], (Fh + [fx])[-(depth + 1):]
+                L = len(Ft) - 1
+                if L > 0:
+                    dF = torch.stack([Ft[k + 1] - Ft[k] for k in range(L)], dim=2)  # [S, 3n, L]
+                    dX = torch.stack([Xt[k + 1] - Xt[k] for k in range(L)], dim=2)
+                    sy = [_aa_system(dF[s], fx[s]) for s in range(S)]
+                    host = torch.cat([dmax.reshape(-1).to(torch.complex128)] + [t for gr in sy for t in gr])
+                    host = host.cpu().numpy()
+                else:
+                    host = dmax.reshape(-1).cpu().numpy()
+                d = np.real(host[:3 * S]).reshape(S, 3)
                 for s in range(S):
                     if res[s] is not None:
                         continue
@@ -412,22 +462,14 @@ def solve_mu_batch_anderson(mus, params: MuParams | None = None, grid: MuGrid | 
                         its[s] = it
                 if all(r is not None for r in res):
                     break
-                Xh.append(x)
-                Fh.append(fx)
-                if len(Fh) > depth + 1:
-                    Xh.pop(0)
-                    Fh.pop(0)
-                if len(Fh) == 1:
+                Xh, Fh = Xt, Ft
+                if L == 0:
                     x = x + beta * fx
                     continue
-                # per solve (batched): gamma = argmin |f - dF gamma|, x <- x + beta f - (dX + beta dF) gamma
-                dF = torch.stack([Fh[k + 1] - Fh[k] for k in range(len(Fh) - 1)], dim=2)  # [S, 3n, L]
-                dX = torch.stack([Xh[k + 1] - Xh[k] for k in range(len(Xh) - 1)], dim=2)
-                gram = dF.conj().transpose(1, 2) @ dF                                     # [S, L, L]
-                tr = torch.real(torch.diagonal(gram, dim1=1, dim2=2).sum(dim=1))
-                gram = gram + (1e-14 * tr + 1e-300)[:, None, None] * torch.eye(gram.shape[1], device=dev)
-                gamma = torch.linalg.solve(gram, (dF.conj().transpose(1, 2) @ fx[:, :, None]))   # [S, L, 1]
-                x = x + beta * fx - ((dX + beta * dF) @ gamma)[:, :, 0]
+                # per solve: gamma = argmin |f - dF gamma|, x <- x + beta f - (dX + beta dF) gamma
+                sys_ = host[3 * S:].reshape(S, L * L + L)
+                gamma = _aa_solve(sys_[:, :L * L].reshape(S, L, L), sys_[:, L * L:])             # [S, L]
+                x = x + beta * fx - _aa_combine(dX, dF, torch.from_numpy(gamma).to(dev), beta)
             for s in range(len(group)):
                 xs = (res[s] if res[s] is not None else x[s]).cpu().numpy()
                 A, B, C = (xs[k * n:(k + 1) * n].reshape(shape).copy() for k in range(3))
