@@ -151,6 +151,13 @@ _PROTOS = [
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, i64p,
                                           ctypes.POINTER(DseErr)]),
     ("dse_mu_sweeper_stats", ctypes.c_int, [ctypes.c_void_p, i64p, i64p, i32p, i64p]),
+    ("dse_mu_aa_residual", ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, i32p, ctypes.c_int32,
+                                          ctypes.c_void_p, f64p, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
+    ("dse_mu_aa_update", ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, i32p, ctypes.c_int32, f64p,
+                                        ctypes.c_double, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
     ("dse_launch_count", ctypes.c_int64, []),
 ]
 

@@ -964,6 +964,100 @@ __global__ void mu_reset_kernel(unsigned* ctr, unsigned long long* err, long lon
     if (t < 4) status[t] = 0;
 }
 
+
+// ---- Anderson acceleration on the device (finite_mu.solve_mu_anderson and
+// solve_mu_batch_anderson).  S solves of N = 3 n_ext complex unknowns each;
+// the last `depth` residual/iterate differences live in ring slots
+// dF[s][slot][N], dX[s][slot][N].  Every reduction is one CTA per output in a
+// fixed order, and every solve is processed by the same code, so a solve
+// batched with others computes bitwise what it computes alone.
+constexpr int kAaMaxDepth = 16;
+constexpr int kAaMaxS = 4;
+struct AaCols {
+    int n;                      // active columns
+    int col[kAaMaxDepth];       // ring slots, oldest first
+    double2 gamma[kAaMaxS][kAaMaxDepth];
+};
+
+// f = gx - x; max |f| per (solve, function) (exact max, order-free);
+// with slot >= 0: dF[slot] = f - fprev, dX[slot] = x - xprev; then fprev = f,
+// xprev = x.
+__global__ void aa_residual_kernel(int S, long long n_ext, const double2* __restrict__ x,
+                                   const double2* __restrict__ gx, double2* __restrict__ f, double2* fprev,
+                                   double2* xprev, double2* __restrict__ dF, double2* __restrict__ dX, int depth,
+                                   int slot, unsigned long long* dmax_bits) {
+    const long long N = 3 * n_ext, total = (long long)S * N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long s = e / N, i = e - s * N;
+        const double2 xv = x[e], gv = gx[e];
+        const double2 fv = make_double2(gv.x - xv.x, gv.y - xv.y);
+        f[e] = fv;
+        const double m = hypot(fv.x, fv.y);
+        atomicMax(dmax_bits + 3 * s + i / n_ext, (unsigned long long)__double_as_longlong(m));
+        if (slot >= 0) {
+            const double2 fp = fprev[e], xp = xprev[e];
+            const size_t o = ((size_t)s * depth + slot) * N + i;
+            dF[o] = make_double2(fv.x - fp.x, fv.y - fp.y);
+            dX[o] = make_double2(xv.x - xp.x, xv.y - xp.y);
+        }
+        fprev[e] = fv;
+        xprev[e] = xv;
+    }
+}
+
+// out[(s * 2 + w) * n + c] = sum_i conj(dF[s][col_c][i]) * v[i] with
+// v = dF[s][slot] (w = 0, the new Gram column) or f[s] (w = 1, the
+// right-hand side); one CTA per (s, w, c), 256 threads, fixed order.
+__global__ void __launch_bounds__(256) aa_dots_kernel(long long n_ext, const double2* __restrict__ f,
+                                                      const double2* __restrict__ dF, int depth, int slot, AaCols cols,
+                                                      double2* __restrict__ out) {
+    __shared__ double2 red[256];
+    const long long N = 3 * n_ext;
+    const int c = blockIdx.x, w = blockIdx.y, s = blockIdx.z;
+    if (w == 0 && slot < 0) return;
+    const double2* a = dF + ((size_t)s * depth + cols.col[c]) * N;
+    const double2* v = w == 0 ? dF + ((size_t)s * depth + slot) * N : f + (size_t)s * N;
+    double re = 0.0, im = 0.0;
+    for (long long i = threadIdx.x; i < N; i += 256) {
+        const double2 p = a[i], q = v[i];
+        re = fma(p.x, q.x, fma(p.y, q.y, re));   // conj(p) q
+        im = fma(p.x, q.y, fma(-p.y, q.x, im));
+    }
+    red[threadIdx.x] = make_double2(re, im);
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if (threadIdx.x < h) {
+            red[threadIdx.x].x += red[threadIdx.x + h].x;
+            red[threadIdx.x].y += red[threadIdx.x + h].y;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[((size_t)s * 2 + w) * cols.n + c] = red[0];
+}
+
+// x <- x + beta f - sum_c gamma_c (dX[col_c] + beta dF[col_c]), the columns in
+// ring order (oldest first).
+__global__ void aa_update_kernel(int S, long long n_ext, double2* __restrict__ x, const double2* __restrict__ f,
+                                 const double2* __restrict__ dF, const double2* __restrict__ dX, int depth,
+                                 double beta, AaCols cols) {
+    const long long N = 3 * n_ext, total = (long long)S * N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long s = e / N, i = e - s * N;
+        double ax = 0.0, ay = 0.0;
+        for (int c = 0; c < cols.n; ++c) {
+            const size_t o = ((size_t)s * depth + cols.col[c]) * N + i;
+            const double2 dx = dX[o], df = dF[o], g = cols.gamma[s][c];
+            const double tx = fma(beta, df.x, dx.x), ty = fma(beta, df.y, dx.y);
+            ax = fma(g.x, tx, fma(-g.y, ty, ax));
+            ay = fma(g.x, ty, fma(g.y, tx, ay));
+        }
+        const double2 xv = x[e], fv = f[e];
+        x[e] = make_double2(fma(beta, fv.x, xv.x) - ax, fma(beta, fv.y, xv.y) - ay);
+    }
+}
+
 }  // namespace mu
 
 struct dse_mu_sweeper {
@@ -1587,6 +1681,76 @@ int dse_mu_sweeper_stats(dse_mu_sweeper* s, int64_t* nominal_points, int64_t* ev
     if (evaluated_points) *evaluated_points = s->evaluated_pairs < 0 ? -1 : s->evaluated_pairs * s->K;
     if (blocks) *blocks = s->blocks;
     if (smem_bytes) *smem_bytes = (int64_t)s->smem;
+    return DSE_OK;
+}
+
+/* Anderson acceleration state kept on the device (see include/dse_b200.h). */
+static int aa_cols(int S, int depth, const int* cols, int ncols, mu::AaCols& c, dse_err* err) {
+    if (S < 1 || S > mu::kAaMaxS || depth < 1 || depth > mu::kAaMaxDepth || ncols < 0 || ncols > depth ||
+        (ncols > 0 && !cols))
+        return fail(err, DSE_EPARAM, "Anderson state: S in 1..%d, depth in 1..%d, ncols <= depth", mu::kAaMaxS,
+                    mu::kAaMaxDepth);
+    c = mu::AaCols{};
+    c.n = ncols;
+    for (int k = 0; k < ncols; ++k) {
+        if (cols[k] < 0 || cols[k] >= depth) return fail(err, DSE_EPARAM, "column slot out of range");
+        c.col[k] = cols[k];
+    }
+    return DSE_OK;
+}
+
+int dse_mu_aa_residual(int32_t S, int64_t n_ext, const double* d_x, const double* d_gx, double* d_f, double* d_fprev,
+                       double* d_xprev, double* d_dF, double* d_dX, int32_t depth, int32_t slot, const int32_t* cols,
+                       int32_t ncols, double* d_scratch, double* host_out, uintptr_t stream, dse_err* err) {
+    ok(err);
+    mu::AaCols c;
+    int rc = aa_cols(S, depth, cols, ncols, c, err);
+    if (rc) return rc;
+    if (n_ext < 1 || !d_x || !d_gx || !d_f || !d_fprev || !d_xprev || !d_scratch || !host_out ||
+        (depth > 0 && (!d_dF || !d_dX)) || slot >= depth)
+        return fail(err, DSE_EPARAM, "bad argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // dots first (16-B aligned), then the delta bits
+    double2* dots = reinterpret_cast<double2*>(d_scratch);
+    unsigned long long* bits = reinterpret_cast<unsigned long long*>(d_scratch + 4 * (size_t)S * ncols);
+    CUDA_TRY(cudaMemsetAsync(bits, 0, sizeof(double) * 3 * S, st));
+    const long long total = (long long)S * 3 * n_ext;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+    mu::aa_residual_kernel<<<blocks, 256, 0, st>>>(S, n_ext, (const double2*)d_x, (const double2*)d_gx,
+                                                   (double2*)d_f, (double2*)d_fprev, (double2*)d_xprev,
+                                                   (double2*)d_dF, (double2*)d_dX, depth, slot, bits);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    if (ncols > 0) {
+        mu::aa_dots_kernel<<<dim3(ncols, 2, S), 256, 0, st>>>(n_ext, (const double2*)d_f, (const double2*)d_dF, depth,
+                                                              slot, c, dots);
+        CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(1);
+    }
+    const size_t bytes = sizeof(double) * (3 * (size_t)S + 4 * (size_t)S * ncols);
+    CUDA_TRY(cudaMemcpyAsync(host_out, d_scratch, bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return DSE_OK;
+}
+
+int dse_mu_aa_update(int32_t S, int64_t n_ext, double* d_x, const double* d_f, const double* d_dF, const double* d_dX,
+                     int32_t depth, const int32_t* cols, int32_t ncols, const double* gamma, double beta,
+                     uintptr_t stream, dse_err* err) {
+    ok(err);
+    mu::AaCols c;
+    int rc = aa_cols(S, depth, cols, ncols, c, err);
+    if (rc) return rc;
+    if (n_ext < 1 || !d_x || !d_f || (ncols > 0 && (!d_dF || !d_dX || !gamma))) return fail(err, DSE_EPARAM, "bad argument");
+    for (int q = 0; q < S; ++q)
+        for (int k = 0; k < ncols; ++k)
+            c.gamma[q][k] = make_double2(gamma[2 * ((size_t)q * ncols + k)], gamma[2 * ((size_t)q * ncols + k) + 1]);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const long long total = (long long)S * 3 * n_ext;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+    mu::aa_update_kernel<<<blocks, 256, 0, st>>>(S, n_ext, (double2*)d_x, (const double2*)d_f, (const double2*)d_dF,
+                                                 (const double2*)d_dX, depth, beta, c);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
     return DSE_OK;
 }
 

@@ -290,18 +290,6 @@ def solve_mu_sharded(params: MuParams | None = None, grid: MuGrid | None = None,
                       history=hist, grid=grid, params=params)
 
 
-def _aa_system(dF, f):
-    """Normal equations of one solve's Anderson step, gamma = argmin
-    |f - dF gamma|: the Gram matrix dF^H dF [L, L] and dF^H f [L], as
-    elementwise products reduced over the 3n axis (a fixed-shape reduction:
-    bandwidth-bound, where a complex GEMM with M = N = L, K = 3n ran at 0.6 ms
-    per call), flattened into one complex vector for a single host copy.
-    dF [3n, L], f [3n] complex.  A solve batched with others forms bitwise the
-    system it forms alone."""
-    cdF = dF.conj()
-    return ((cdF[:, :, None] * dF[:, None, :]).sum(dim=0).reshape(-1), (cdF * f[:, None]).sum(dim=0))
-
-
 def _aa_solve(gram: np.ndarray, rhs: np.ndarray) -> np.ndarray:
     """The L x L regularised solve on the host (LAPACK, one small matrix per
     solve: identical alone or stacked), gram [..., L, L], rhs [..., L]."""
@@ -311,15 +299,70 @@ def _aa_solve(gram: np.ndarray, rhs: np.ndarray) -> np.ndarray:
     return np.linalg.solve(reg, rhs[..., None])[..., 0]
 
 
-def _aa_combine(dX, dF, gamma, beta):
-    """(dX + beta dF) @ gamma as an explicit fixed-order sum over the L columns
-    (elementwise: identical for a solve alone and in a batch).  dX, dF
-    [..., 3n, L]; gamma [..., L]."""
-    acc = None
-    for k in range(dF.shape[-1]):
-        t = (dX[..., k] + beta * dF[..., k]) * gamma[..., k:k + 1]
-        acc = t if acc is None else acc + t
-    return acc
+class _DeviceAnderson:
+    """Anderson acceleration state of S solves on the device (dse_mu_aa_*):
+    the last `depth` residual and iterate differences in ring slots, the
+    residual, deltas, new Gram column and right-hand side formed by two
+    kernels and copied to the host in one transfer per sweep; the Gram matrix
+    is kept on the host (one new column per sweep) and the depth x depth
+    system solved there (_aa_solve); the update is one kernel.  Every solve is
+    processed by the same per-solve code: a solve batched with others is
+    bitwise its standalone run."""
+
+    def __init__(self, S: int, n_ext: int, depth: int, beta: float, dev, stream: int):
+        import torch
+        if not 1 <= depth <= 16:
+            raise ParameterError("Anderson depth must be in 1..16")
+        self.S, self.n, self.depth, self.beta, self.stream = S, n_ext, depth, float(beta), stream
+        N = 3 * n_ext
+
+        def z(*shape):
+            return torch.zeros(shape, dtype=torch.complex128, device=dev)
+        self.f, self.fprev, self.xprev = z(S, N), z(S, N), z(S, N)
+        self.dF, self.dX = z(S, depth, N), z(S, depth, N)
+        self.scratch = torch.zeros(3 * S + 4 * S * depth, dtype=torch.float64, device=dev)
+        self.host = np.zeros(3 * S + 4 * S * depth)
+        self.G = np.zeros((S, depth, depth), dtype=np.complex128)
+        self.count = 0          # differences formed so far
+        self.started = False
+        self.cols = np.zeros(0, dtype=np.int32)
+        self.rhs = None
+        self.lib = nat.load()
+
+    def residual(self, x, gx) -> np.ndarray:
+        """f = gx - x and the new difference; returns max |f| [S, 3] (A, B, C)."""
+        S, depth = self.S, self.depth
+        slot = -1
+        if self.started:
+            slot = self.count % depth
+            self.count += 1
+        L = min(self.count, depth)
+        self.cols = np.array([(self.count - L + k) % depth for k in range(L)], dtype=np.int32)
+        err = nat.DseErr()
+        nat.raise_for(self.lib.dse_mu_aa_residual(
+            S, self.n, x.data_ptr(), gx.data_ptr(), self.f.data_ptr(), self.fprev.data_ptr(), self.xprev.data_ptr(),
+            self.dF.data_ptr(), self.dX.data_ptr(), depth, slot, self.cols.ctypes.data_as(nat.i32p), L,
+            self.scratch.data_ptr(), self.host.ctypes.data_as(nat.f64p), self.stream, ctypes.byref(err)), err)
+        self.started = True
+        if L:
+            c = self.host[:4 * S * L].view(np.complex128).reshape(S, 2, L)
+            for k, col in enumerate(self.cols):
+                self.G[:, slot, col] = np.conj(c[:, 0, k])
+                self.G[:, col, slot] = c[:, 0, k]
+            self.rhs = c[:, 1, :].copy()
+        return self.host[4 * S * L:4 * S * L + 3 * S].reshape(S, 3).copy()
+
+    def update(self, x) -> None:
+        """x <- x + beta f - (dX + beta dF) gamma, in place."""
+        L = len(self.cols)
+        gamma = np.zeros((self.S, 0), dtype=np.complex128)
+        if L:
+            gamma = np.ascontiguousarray(_aa_solve(self.G[:, self.cols][:, :, self.cols], self.rhs))
+        err = nat.DseErr()
+        nat.raise_for(self.lib.dse_mu_aa_update(
+            self.S, self.n, x.data_ptr(), self.f.data_ptr(), self.dF.data_ptr(), self.dX.data_ptr(), self.depth,
+            self.cols.ctypes.data_as(nat.i32p), L, gamma.view(np.float64).ctypes.data_as(nat.f64p), self.beta,
+            self.stream, ctypes.byref(err)), err)
 
 
 def solve_mu_anderson(params: MuParams | None = None, grid: MuGrid | None = None, a0=None, b0=None, c0=None,
@@ -353,43 +396,24 @@ def solve_mu_anderson(params: MuParams | None = None, grid: MuGrid | None = None
     own = sweeper is None
     sw = MuSweeper(grid, params, device) if own else sweeper
     hist = [MuIterationRecord(0, float("nan"), float("nan"), float("nan"))]
-    X, F = [], []
     converged, n_it = False, params.max_iterations
     try:
         st = torch.cuda.current_stream(dev).cuda_stream
         err = nat.DseErr()
+        aa = _DeviceAnderson(1, n, depth, beta, dev, st)
         for it in range(1, params.max_iterations + 1):
             nat.raise_for(lib.dse_mu_solve_load(sw.handle, x[:n].data_ptr(), x[n:2 * n].data_ptr(),
                                                 x[2 * n:].data_ptr(), st, ctypes.byref(err)), err)
             nat.raise_for(lib.dse_mu_sharded_sweep_pack(sw.handle, ctypes.byref(cp), send.data_ptr(), n, st,
                                                         ctypes.byref(err)), err)
             nat.raise_for(lib.dse_mu_sharded_failure(sw.handle, st, ctypes.byref(err)), err)
-            f = send - x
-            dmax = f.view(3, n).abs().amax(dim=1)
-            # the Anderson system with this residual appended is formed before
-            # the stop test, so that the deltas and the system reach the host
-            # in one copy (one sync per sweep)
-            Xt, Ft = (X + [x.clone()])[-(depth + 1):], (F + [f])[-(depth + 1):]
-            if len(Ft) > 1:
-                dF = torch.stack([Ft[k + 1] - Ft[k] for k in range(len(Ft) - 1)], dim=1)
-                dX = torch.stack([Xt[k + 1] - Xt[k] for k in range(len(Xt) - 1)], dim=1)
-                g_, r_ = _aa_system(dF, f)
-                host = torch.cat([dmax.to(torch.complex128), g_, r_]).cpu().numpy()
-            else:
-                host = dmax.cpu().numpy()
-            d = np.real(host[:3])
+            d = aa.residual(x, send)[0]
             hist.append(MuIterationRecord(it, float(d[0]), float(d[1]), float(d[2])))
             if d[0] < params.xi and d[1] < params.xi and d[2] < params.xi:
                 x = send.clone()
                 converged, n_it = True, it
                 break
-            X, F = Xt, Ft
-            if len(F) == 1:
-                x = x + beta * f
-                continue
-            L = len(F) - 1
-            gamma = _aa_solve(host[3:3 + L * L].reshape(L, L), host[3 + L * L:])
-            x = x + beta * f - _aa_combine(dX, dF, torch.from_numpy(gamma).to(dev), beta)
+            aa.update(x)
     finally:
         if own:
             sw.close()
@@ -427,7 +451,7 @@ def solve_mu_batch_anderson(mus, params: MuParams | None = None, grid: MuGrid | 
                 _check_c_projection(grid, p_)
             x = init.repeat(S, 1).contiguous()
             gx = torch.empty_like(x)
-            Xh, Fh = [], []  # histories as [S, 3n] tensors: the AA algebra is batched over the group
+            aa = _DeviceAnderson(S, n, depth, beta, dev, torch.cuda.current_stream(dev).cuda_stream)
             hist = [[MuIterationRecord(0, float("nan"), float("nan"), float("nan"))] for _ in range(S)]
             res = [None] * S
             its = [params.max_iterations] * S
@@ -438,21 +462,7 @@ def solve_mu_batch_anderson(mus, params: MuParams | None = None, grid: MuGrid | 
                         from .errors import NumericalFailureError
                         raise NumericalFailureError(f"non-finite integrand in batched finite-mu sweep, mu="
                                                     f"{plist[s].mu}, row={failed[s]}", row=failed[s], iteration=it)
-                fx = gx - x
-                dmax = fx.view(S, 3, n).abs().amax(dim=2)
-                # the Anderson systems with this residual appended are formed
-                # before the stop test: deltas and systems in one host copy
-                Xt, Ft = (Xh + [x])[-(depth + 1):], (Fh + [fx])[-(depth + 1):]
-                L = len(Ft) - 1
-                if L > 0:
-                    dF = torch.stack([Ft[k + 1] - Ft[k] for k in range(L)], dim=2)  # [S, 3n, L]
-                    dX = torch.stack([Xt[k + 1] - Xt[k] for k in range(L)], dim=2)
-                    sy = [_aa_system(dF[s], fx[s]) for s in range(S)]
-                    host = torch.cat([dmax.reshape(-1).to(torch.complex128)] + [t for gr in sy for t in gr])
-                    host = host.cpu().numpy()
-                else:
-                    host = dmax.reshape(-1).cpu().numpy()
-                d = np.real(host[:3 * S]).reshape(S, 3)
+                d = aa.residual(x, gx)
                 for s in range(S):
                     if res[s] is not None:
                         continue
@@ -462,14 +472,7 @@ def solve_mu_batch_anderson(mus, params: MuParams | None = None, grid: MuGrid | 
                         its[s] = it
                 if all(r is not None for r in res):
                     break
-                Xh, Fh = Xt, Ft
-                if L == 0:
-                    x = x + beta * fx
-                    continue
-                # per solve: gamma = argmin |f - dF gamma|, x <- x + beta f - (dX + beta dF) gamma
-                sys_ = host[3 * S:].reshape(S, L * L + L)
-                gamma = _aa_solve(sys_[:, :L * L].reshape(S, L, L), sys_[:, L * L:])             # [S, L]
-                x = x + beta * fx - _aa_combine(dX, dF, torch.from_numpy(gamma).to(dev), beta)
+                aa.update(x)
             for s in range(len(group)):
                 xs = (res[s] if res[s] is not None else x[s]).cpu().numpy()
                 A, B, C = (xs[k * n:(k + 1) * n].reshape(shape).copy() for k in range(3))

@@ -335,3 +335,47 @@ def test_narrow_interaction_skip_windows(vertex):
         sw.solve(MuParams(**{**pm.__dict__, "max_iterations": 1}))
         st = sw.stats()
     assert 0 < st["evaluated_points"] < st["nominal_points"] // 4, st
+
+
+def test_device_anderson_kernels_match_numpy():
+    """dse_mu_aa_residual / dse_mu_aa_update (the device Anderson state) against
+    a numpy restatement of the same step on random data: residual maxima
+    bitwise, Gram columns and right-hand sides to rounding, the ring order of
+    the columns, and the update x + beta f - (dX + beta dF) gamma."""
+    import torch
+    from paper_2012_03667_b200.finite_mu import _DeviceAnderson, _aa_solve
+    rng = np.random.default_rng(5)
+    S, n, depth, beta = 2, 50, 3, 0.7
+    dev = torch.device("cuda", 0)
+    aa = _DeviceAnderson(S, n, depth, beta, dev, 0)
+    x = torch.from_numpy(rng.standard_normal((S, 3 * n)) + 1j * rng.standard_normal((S, 3 * n))).to(dev)
+    X, F = [], []
+    for step in range(6):
+        gx_h = x.cpu().numpy() + 0.5 ** step * (rng.standard_normal((S, 3 * n)) + 1j * rng.standard_normal((S, 3 * n)))
+        gx = torch.from_numpy(gx_h).to(dev)
+        xh = x.cpu().numpy()
+        f = gx_h - xh
+        d = aa.residual(x, gx)
+        ref_d = np.abs(f).reshape(S, 3, n).max(axis=2)
+        assert np.allclose(d, ref_d, rtol=1e-15, atol=0)
+        X.append(xh)
+        F.append(f)
+        X, F = X[-(depth + 1):], F[-(depth + 1):]
+        L = len(F) - 1
+        assert len(aa.cols) == L
+        if L:
+            dF = np.stack([F[k + 1] - F[k] for k in range(L)], axis=2)   # oldest first
+            dX = np.stack([X[k + 1] - X[k] for k in range(L)], axis=2)
+            G = np.einsum("sik,sil->skl", dF.conj(), dF)
+            rhs = np.einsum("sik,si->sk", dF.conj(), f)
+            got_G = aa.G[:, aa.cols][:, :, aa.cols]
+            assert np.max(np.abs(got_G - G)) <= 1e-12 * np.max(np.abs(G))
+            assert np.max(np.abs(aa.rhs - rhs)) <= 1e-12 * np.max(np.abs(rhs))
+            gamma = _aa_solve(got_G, aa.rhs)
+            ref_x = xh + beta * f - np.einsum("sik,sk->si", dX + beta * dF, gamma)
+        else:
+            ref_x = xh + beta * f
+        aa.update(x)
+        torch.cuda.synchronize()
+        got = x.cpu().numpy()
+        assert np.max(np.abs(got - ref_x)) <= 1e-12 * np.max(np.abs(ref_x))
