@@ -806,6 +806,9 @@ __global__ void __launch_bounds__(kThreads, MOM ? DSE_MU_MOM_MINB : DSE_MU_MINB)
 // and coefficient); the per-solve arithmetic and reduction order are those of
 // mu_solve_kernel<V, true>, so each solve's sweep is bitwise its standalone
 // moments-mode sweep.
+// (rejected: cp.async staging of the next pair as in mu_solve_kernel<V, true>
+// -- moments only for S = 4, moments + both node tables for S = 2 -- measured
+// slower, S = 2 2.73 -> 3.15 ms, S = 4 5.02 -> 5.32 ms per sweep)
 constexpr int kMuMaxBatch = 4;
 struct MuBatch {
     const double2* Xin;   // [S][3][n_ext]
