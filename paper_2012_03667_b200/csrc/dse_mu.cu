@@ -209,6 +209,10 @@ __device__ __forceinline__ void pair_moments(const MuArgs& a, const RowC& rc, in
 // (fewer operations: config 3 direct 5.16 -> 5.13 ms, batched S=4 5.11 ->
 // 5.01 ms).  With the trimmed zero terms and rcp_pair, 5.28 -> 5.13 ms direct,
 // 2.06 -> 1.83 ms moments, 5.59 -> 5.01 ms batched (S=4).
+#ifndef DSE_MU_FACTORED
+#define DSE_MU_FACTORED 1  // regrouped A/C channels for the vertices without Delta_A/Delta_C
+#endif
+constexpr bool kMuFactored = DSE_MU_FACTORED;
 #ifndef DSE_MU_LATE_B
 #define DSE_MU_LATE_B 1
 #endif
@@ -250,31 +254,53 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
     constexpr bool fb = V != DSE_MU_VERTEX_BC1;
     constexpr bool fdb = V == DSE_MU_VERTEX_BC;
     const cplx zero = C(0.0, 0.0);
-    // A channel (e = p_vec): F_A = cA00 + cA01 r + K (cA10 + cA11 r + cA12 r^2)
-    const cplx lam0 = akQp + sA * akQ;
-    const cplx cA00 = fac ? (-0.5 * P2) * (nu0 + dA * eta0) : zero;
-    cplx cA01 = Aq * sC;  // Aq tau0 - 2 sA Aq
-    cplx cA10 = (-P2) * lam0;
-    cplx cA11 = lam0 + (2.0 * P2) * sAAq + Aq * tau1;
-    if (fac) {
-        cA01 = cA01 - 0.5 * (nu0 + P2 * nu1 - Aq * delta0 + dA * (eta0 + P2 * Aq));
-        cA10 = cA10 - (0.5 * P2) * (kt * (nu0 - dA * akQ));
-        cA11 = cA11 - 0.5 * (kt * (P2 * nu1 - nu0) + Aq * psi + (dA * kt) * (P2 * Aq - akQ));
-    }
-    const cplx cA12 = -2.0 * sAAq;
-    // C channel (e = unit 4): F_C = cC00 + cC01 r + K (cC10 + cC11 r)
-    const cplx lam0c = akQp + sC * akQ;
-    const cplx lam1c = (sA + sC) * Aq;
-    const cplx dCt4 = dC * t4;
-    cplx cC00 = Cq_q4t * (tau0 - 2.0 * sC);
-    cplx cC01 = zero;
-    cplx cC10 = k4 * lam0c + Cq_q4t * tau1;
-    cplx cC11 = (-k4) * lam1c;
-    if (fac) {
-        cC00 = cC00 - 0.5 * (t4 * nu0 - Cq_q4t * delta0 + dCt4 * eta0);
-        cC01 = -0.5 * (t4 * nu1 - 2.0 * (Cq_q4t * dA) + dCt4 * Aq);
-        cC10 = cC10 - 0.5 * (Cq_q4t * psi - kt * (k4 * nu0 + dCt4 * akQ));
-        cC11 = cC11 - 0.5 * (kt * (dCt4 * Aq - k4 * nu1));
+    cplx FA, FC;
+    if constexpr (!fac && kMuFactored) {
+        // without the Delta_A/Delta_C parts the A and C channels regroup over
+        // moment combinations (exact algebra on the general form below):
+        //   F_A = Aq sC S1 + lam0 (T1 - P2 T0) + sA Aq 2 (P2 T1 - T2) + Aq tau1 T1
+        //   F_C = Cq q~4 ((2 sA - sC) S0 + k4^2 (sA + sC) T0) + k4 (Q2 T0 - T1) (sA + sC) Aq
+        // with lam0 = 2 Q2 sA Aq + k4 (sA + sC) Cq q~4
+        const cplx ssum = sA + sC;
+        const double k42 = k4 * k4;
+        const cplx lam0 = (2.0 * Q2) * sAAq + k4 * (ssum * Cq_q4t);
+        const double U = fma(-P2, T0, T1);
+        const double Vv = 2.0 * fma(P2, T1, -T2);
+        const double W = fma(Q2, T0, -T1);
+        FA = cfma(Aq * sC, S1, cfma(lam0, U, cfma(sAAq, Vv, T1 * (Aq * tau1))));
+        FC = Cq_q4t * cfma(2.0 * sA - sC, S0, (k42 * T0) * ssum) + (k4 * W) * (ssum * Aq);
+    } else {
+        // A channel (e = p_vec): F_A = cA00 + cA01 r + K (cA10 + cA11 r + cA12 r^2)
+        const cplx lam0 = akQp + sA * akQ;
+        const cplx cA00 = fac ? (-0.5 * P2) * (nu0 + dA * eta0) : zero;
+        cplx cA01 = Aq * sC;  // Aq tau0 - 2 sA Aq
+        cplx cA10 = (-P2) * lam0;
+        cplx cA11 = lam0 + (2.0 * P2) * sAAq + Aq * tau1;
+        if (fac) {
+            cA01 = cA01 - 0.5 * (nu0 + P2 * nu1 - Aq * delta0 + dA * (eta0 + P2 * Aq));
+            cA10 = cA10 - (0.5 * P2) * (kt * (nu0 - dA * akQ));
+            cA11 = cA11 - 0.5 * (kt * (P2 * nu1 - nu0) + Aq * psi + (dA * kt) * (P2 * Aq - akQ));
+        }
+        const cplx cA12 = -2.0 * sAAq;
+        // C channel (e = unit 4): F_C = cC00 + cC01 r + K (cC10 + cC11 r)
+        const cplx lam0c = akQp + sC * akQ;
+        const cplx lam1c = (sA + sC) * Aq;
+        const cplx dCt4 = dC * t4;
+        cplx cC00 = Cq_q4t * (tau0 - 2.0 * sC);
+        cplx cC01 = zero;
+        cplx cC10 = k4 * lam0c + Cq_q4t * tau1;
+        cplx cC11 = (-k4) * lam1c;
+        if (fac) {
+            cC00 = cC00 - 0.5 * (t4 * nu0 - Cq_q4t * delta0 + dCt4 * eta0);
+            cC01 = -0.5 * (t4 * nu1 - 2.0 * (Cq_q4t * dA) + dCt4 * Aq);
+            cC10 = cC10 - 0.5 * (Cq_q4t * psi - kt * (k4 * nu0 + dCt4 * akQ));
+            cC11 = cC11 - 0.5 * (kt * (dCt4 * Aq - k4 * nu1));
+        }
+
+        const cplx FA0 = cfma(cA01, S1, cfma(cA10, T0, cfma(cA11, T1, T2 * cA12)));
+        FA = fac ? cfma(cA00, S0, FA0) : FA0;
+        const cplx FC0 = cfma(cC10, T0, T1 * cC11);
+        FC = cfma(cC00, S0, fac ? cfma(cC01, S1, FC0) : FC0);
     }
     // B channel: F_B = cB00 + cB01 r + K (cB10 + cB11 r); without Delta_B
     // every coefficient carries the factor Bq, which is applied once (with
@@ -304,10 +330,6 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
     // (terms whose coefficient is identically zero for this vertex are not
     // formed: 0 * moment would only matter for a non-finite moment, and a
     // non-finite moment already makes the other terms non-finite)
-    const cplx FA0 = cfma(cA01, S1, cfma(cA10, T0, cfma(cA11, T1, T2 * cA12)));
-    const cplx FA = fac ? cfma(cA00, S0, FA0) : FA0;
-    const cplx FC0 = cfma(cC10, T0, T1 * cC11);
-    const cplx FC = cfma(cC00, S0, fac ? cfma(cC01, S1, FC0) : FC0);
     const cplx FB0 = fdb ? cfma(cB10, T0, T1 * cB11) : T0 * cB10;
     const cplx FB = cfma(cB00, S0, fb ? cfma(cB01, S1, FB0) : FB0);
     const double sc = rc.coeff * (__ldg(a.meas_s + js) * __ldg(a.meas_4 + j4));
