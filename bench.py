@@ -519,8 +519,8 @@ def interp_bench(p, nat, torch, dev, hbm):
     return res
 
 
-# ncu SASS mix of mu_solve_kernel<bcb> (profiles/r01/mu_sweep.md, a79d8c1): 2*DFMA + DMUL + DADD per evaluated point
-MU_FLOP_PER_POINT = 43.75
+# ncu SASS mix of mu_solve_kernel<bcb> (profiles/r01/mu_sweep.md, final round-1 build): 2*DFMA + DMUL + DADD per evaluated point
+MU_FLOP_PER_POINT = 42.57
 
 
 def mu_cpu_rate(budget_s: float):
