@@ -133,7 +133,9 @@ __device__ void build_nodes(const MuArgs& a, const double2* __restrict__ Xin, in
         const cplx Aq = C(v[0].x, v[0].y), Bq = C(v[1].x, v[1].y), Cq = C(v[2].x, v[2].y);
         const cplx q4t = C(a.q4[j4], a.mu);
         const cplx den = a.Q2[js] * (Aq * Aq) + (q4t * q4t) * (Cq * Cq) + Bq * Bq;
-        cplx r = rcp(den);
+        // 1/den with the pair weight's node factors folded in: coeff * (meas_s
+        // meas_4) / den, the same two roundings the contraction applied per pair
+        cplx r = (a.coeff * (__ldg(a.meas_s + js) * __ldg(a.meas_4 + j4))) * rcp(den);
         // a non-finite node poisons 1/den so that no pair using it is skipped
         // (the oracle's 0 * NaN = NaN flags it at every angle)
         if (!isfinite(v[0].x + v[0].y + v[1].x + v[1].y + v[2].x + v[2].y + r.x + r.y)) {
@@ -165,6 +167,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 struct RowC {
     double P, P2, p4r;
     cplx p4t, Ap, Bp, Cp;
+    cplx hAp, hCp;     // Ap / 2, Cp / 2 (exact): s_A = fma(1/2, Aq, Ap / 2) == (Ap + Aq) / 2 bitwise
     double mu, coeff;  // per solve (batched sweeps carry several)
 };
 
@@ -233,7 +236,8 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
     // experiment hook (DSE_MU_DQ_EPS2, default 0 = the exact quotient):
     // Tikhonov-regularised 1/(q~^2 - p~^2) = conj(d) / (|d|^2 + eps^2)
     const cplx rkt = a.dq_eps2 > 0.0 ? (1.0 / fma(kt.x, kt.x, fma(kt.y, kt.y, a.dq_eps2))) * C(kt.x, -kt.y) : rcp_pair(kt);
-    const cplx sA = 0.5 * (rc.Ap + Aq), sC = 0.5 * (rc.Cp + Cq);
+    const cplx sA = C(fma(0.5, Aq.x, rc.hAp.x), fma(0.5, Aq.y, rc.hAp.y));
+    const cplx sC = C(fma(0.5, Cq.x, rc.hCp.x), fma(0.5, Cq.y, rc.hCp.y));
     const cplx dA = (Aq - rc.Ap) * rkt, dC = (Cq - rc.Cp) * rkt, dB = (Bq - rc.Bp) * rkt;
     const cplx tau0 = 2.0 * sA + sC;
     const cplx tau1 = (k4 * k4) * (sA - sC);
@@ -332,8 +336,7 @@ __device__ __forceinline__ void pair_contract(const MuArgs& a, const RowC& rc, i
     // non-finite moment already makes the other terms non-finite)
     const cplx FB0 = fdb ? cfma(cB10, T0, T1 * cB11) : T0 * cB10;
     const cplx FB = cfma(cB00, S0, fb ? cfma(cB01, S1, FB0) : FB0);
-    const double sc = rc.coeff * (__ldg(a.meas_s + js) * __ldg(a.meas_4 + j4));
-    const cplx rd = sc * C(vR.x, vR.y);
+    const cplx rd = C(vR.x, vR.y);  // coeff * meas / den (build_nodes)
     const cplx gA = FA * rd, gB = FB * (late_b ? Bq * rd : rd), gC = FC * rd;
     acc[0] += gA.x; acc[1] += gA.y;
     acc[2] += gB.x; acc[3] += gB.y;
@@ -469,6 +472,8 @@ __device__ __forceinline__ RowC row_consts(const MuArgs& a, const double2* Xin, 
     rc.Ap = C(va.x, va.y);
     rc.Bp = C(vb.x, vb.y);
     rc.Cp = C(vc.x, vc.y);
+    rc.hAp = 0.5 * rc.Ap;
+    rc.hCp = 0.5 * rc.Cp;
     rc.mu = a.mu;
     rc.coeff = a.coeff;
     return rc;
@@ -856,6 +861,7 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_batch_kernel(MuArgs 
     for (int s = 0; s < S; ++s) {
         MuArgs as = a;
         as.mu = b.mu[s];
+        as.coeff = b.coeff[s];
         as.NB = b.NB + (size_t)s * 4 * m_int;
         build_nodes(as, b.Xin + (size_t)s * 3 * n_ext, b.nonfinite + s);
     }
@@ -960,6 +966,8 @@ __global__ void __launch_bounds__(kThreads) mu_locate_kernel(MuArgs a, int i, in
     rc.Ap = C(Xin[i].x, Xin[i].y);
     rc.Bp = C(Xin[n_ext + i].x, Xin[n_ext + i].y);
     rc.Cp = C(Xin[2 * n_ext + i].x, Xin[2 * n_ext + i].y);
+    rc.hAp = 0.5 * rc.Ap;
+    rc.hCp = 0.5 * rc.Cp;
     rc.mu = a.mu;
     rc.coeff = a.coeff;
     // per point: run the pair form with a single-angle weight table
