@@ -52,6 +52,12 @@ constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
 // is FP64-pipe bound, not add-chain bound)
 // (an 11-bit exp table with a degree-3 polynomial ran 0.333 ms but put a
 // config-2 random-state sweep at 1.1e-12 of the oracle: kept at 8 bits, degree 4)
+// (fewer accumulators: with r = (psum - kappa)/2 and rho kappa = 1, T1 =
+// (psum T0 - S0)/2, T2 = (psum T1 - S1)/2, even S1 = (psum S0 - sum ew)/2 --
+// 3 to 4 FP64 instructions fewer per point, but a numpy model against long
+// double puts the A channel 5-20x further from the exact sums (1.6e-11 to
+// 6e-11 vs 3e-12 at config 0): the subtraction reintroduces the cancellation
+// that accumulating r-weighted moments avoids.  Not built.)
 
 __global__ void __launch_bounds__(kPairsThreads, DSE_PAIRS_MINB) dse_pairs_kernel(SweepArgs a) {
     cg::grid_group grid = cg::this_grid();
