@@ -49,3 +49,31 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"import\s+oracle|from\s+oracle|liboracle_dse|dse_oracle", txt), f
+
+
+def test_anderson_state_argument_validation_without_gpu():
+    """dse_mu_aa_residual / dse_mu_aa_update reject bad shapes before any CUDA
+    call (DSE_EPARAM -> ParameterError), and the Python state checks the
+    depth the kernels support (1..16)."""
+    from paper_2012_03667_b200.errors import ParameterError
+    from paper_2012_03667_b200.finite_mu import _DeviceAnderson
+    lib = _native.load()
+    err = _native.DseErr()
+    cols = (ctypes.c_int32 * 4)(0, 1, 2, 3)
+    host = np.zeros(64)
+    hp = host.ctypes.data_as(_native.f64p)
+    # S = 5 solves (max 4), depth 17 (max 16), ncols > depth
+    for S, depth, slot, ncols in ((5, 4, 0, 1), (1, 17, 0, 1), (1, 2, 0, 3), (1, 2, 0, 4)):
+        rc = lib.dse_mu_aa_residual(S, 8, 1, 1, 1, 1, 1, 1, 1, depth, slot, cols, ncols, 1, hp, 0, ctypes.byref(err))
+        assert rc == _native.DSE_EPARAM, (S, depth, ncols)
+        rc = lib.dse_mu_aa_update(S, 8, 1, 1, 1, 1, depth, cols, ncols, hp, 1.0, 0, ctypes.byref(err))
+        assert rc == _native.DSE_EPARAM
+    bad_cols = (ctypes.c_int32 * 2)(0, 5)  # slot 5 of a depth-2 ring
+    rc = lib.dse_mu_aa_residual(1, 8, 1, 1, 1, 1, 1, 1, 1, 2, 0, bad_cols, 2, 1, hp, 0, ctypes.byref(err))
+    assert rc == _native.DSE_EPARAM and b"slot" in err.msg
+    # null state pointers
+    rc = lib.dse_mu_aa_residual(1, 8, None, 1, 1, 1, 1, 1, 1, 2, -1, cols, 0, 1, hp, 0, ctypes.byref(err))
+    assert rc == _native.DSE_EPARAM and err.msg
+    for depth in (0, 17):
+        with pytest.raises(ParameterError):
+            _DeviceAnderson(1, 8, depth, 1.0, "cpu", 0)
