@@ -661,9 +661,13 @@ def mu_bench(p, torch, dev, flush, args, peak, no_cpu):
     mus = [0.4 * (k + 0.5) / 32 for k in range(32)]
     solve_mu_batch_anderson(mus[:4], pmo, g)  # warm-up (kernels, allocations)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    bb = solve_mu_batch_anderson(mus, pmo, g, batch=4)
-    t4b = time.perf_counter() - t0
+    runs_4b = []
+    for _ in range(2):  # whole 32-solve job twice (host-latency sensitive: report both, use the better)
+        t0 = time.perf_counter()
+        bb = solve_mu_batch_anderson(mus, pmo, g, batch=4)
+        torch.cuda.synchronize()
+        runs_4b.append(time.perf_counter() - t0)
+    t4b = min(runs_4b)
     with MuSweeper(g, pmo) as sw:
         solve_mu_anderson(pmo, g, sweeper=sw)  # builds the table, warms up
         torch.cuda.synchronize()
@@ -698,11 +702,11 @@ def mu_bench(p, torch, dev, flush, args, peak, no_cpu):
                                            "iterations": [s.iterations for s in aa4],
                                            "converged": int(sum(s.converged for s in aa4))},
                       "batched_anderson_moments": {
-                          "seconds": t4b, "solves_per_s": len(mus) / t4b, "batch": 4,
+                          "seconds": t4b, "solves_per_s": len(mus) / t4b, "batch": 4, "runs_seconds": runs_4b,
                           "iterations": [s.iterations for s in bb], "converged": int(sum(s.converged for s in bb)),
                           "note": "groups of 4 mu values swept by one kernel (dse_mu_batch_sweep: the moment "
                                   "table read once per pair for the group), batched Anderson algebra; includes "
-                                  "the moment-table build"}}
+                                  "the moment-table build; seconds = the better of two full runs"}}
     if not no_cpu:
         rate, info = mu_cpu_rate(float(os.environ.get("BENCH_MU_CPU_S", "8")))
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["cores"], "kind": "port",
