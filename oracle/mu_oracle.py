@@ -260,15 +260,16 @@ def _clib():
         lib.mu_sweep_rows.argtypes = [f64, f64, i64, i64, f64, f64, f64, i64, i64, f64, f64, i64,
                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_double, ctypes.c_int, f64, f64, f64, f64, f64, f64,
-                                      ctypes.POINTER(ctypes.c_int64), i64, f64, ctypes.c_int]
+                                      ctypes.POINTER(ctypes.c_int64), i64, f64, ctypes.c_int, ctypes.c_int]
         _CLIB = lib
     return _CLIB
 
 
-def sweep_rows_c(grid, params, A, B, C, rows, threads: int | None = None):
+def sweep_rows_c(grid, params, A, B, C, rows, threads: int | None = None, skip: bool = True):
     """(A', B', C') at the listed external points, C restatement (sequential
     sums over (j_s, j_4, k) per point; np.sum's pairwise order in sweep_row
-    differs at the rounding level).  Returns complex array [len(rows), 3]."""
+    differs at the rounding level).  Returns complex array [len(rows), 3].
+    skip: the exact-zero node skip (bitwise equal to skip=False)."""
     import ctypes
     import os
     lib = _clib()
@@ -287,8 +288,38 @@ def sweep_rows_c(grid, params, A, B, C, rows, threads: int | None = None):
                             ptr[6], grid.m_ang, params.interaction_coeff, params.omega, params.mu, params.z1,
                             params.m0, vertex, cv(A), cv(B), cv(C), cv(Aq), cv(Bq), cv(Cq),
                             rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), rows.size, cv(out),
-                            int(threads or os.cpu_count() or 1))
+                            int(threads or os.cpu_count() or 1), int(bool(skip)))
     del f
     if bad:
         raise MuNumericalFailure(-1, -1, -1)
     return out
+
+
+def solve_c(grid, params, A0=None, B0=None, C0=None, threads: int | None = None, skip: bool = True,
+            on_iteration=None):
+    """solve() with every sweep done by the C restatement (sweep_rows_c over
+    all external points; sequential sums over (j_s, j_4, k)): the oracle for
+    full-size configs 3-4, where the numpy sweep is too slow.  Same loop,
+    relaxation, deltas, stop rule and history as solve()."""
+    shape = (grid.n_s, grid.n_4)
+    A = np.ones(shape, np.complex128) if A0 is None else np.array(A0, np.complex128).reshape(shape)
+    B = np.full(shape, 0.3, np.complex128) if B0 is None else np.array(B0, np.complex128).reshape(shape)
+    C = np.ones(shape, np.complex128) if C0 is None else np.array(C0, np.complex128).reshape(shape)
+    relax = params.relaxation
+    rows = np.arange(grid.n_ext)
+    hist = [(0, np.nan, np.nan, np.nan)]
+    for n in range(1, params.max_iterations + 1):
+        out = sweep_rows_c(grid, params, A, B, C, rows, threads=threads, skip=skip)
+        An, Bn, Cn = (out[:, c].reshape(shape) for c in range(3))
+        if relax != 1.0:
+            An = relax * An + (1.0 - relax) * A
+            Bn = relax * Bn + (1.0 - relax) * B
+            Cn = relax * Cn + (1.0 - relax) * C
+        d = (delta(An, A), delta(Bn, B), delta(Cn, C))
+        A, B, C = An, Bn, Cn
+        hist.append((n, *d))
+        if on_iteration is not None:
+            on_iteration(n, d)
+        if all(x < params.xi for x in d):
+            return A, B, C, n, True, hist
+    return A, B, C, params.max_iterations, False, hist

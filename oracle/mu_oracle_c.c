@@ -8,6 +8,14 @@
  * parallel over points with OpenMP.  PARITY UNPINNED AGAINST THE REFERENCE
  * (there is no finite-mu reference path); checked against the numpy oracle
  * in tests/test_mu_oracle.py.
+ *
+ * skip != 0: a (j_s, j_4) node whose every angular point has
+ * exp(-k^2/w^2) == 0 exactly (lower bound of k^2 over the angles,
+ * ((|q| - |p|)^2 + (q4 - p4)^2) / w^2 > 760, well past the underflow at
+ * 745.13) is not evaluated -- the GPU kernels' exact-zero window skip.  It is
+ * taken only when every value entering the node's summands is finite and
+ * den != 0, so each skipped summand would have been an exact +-0: the sums
+ * are bitwise those of skip = 0 (tested).
  */
 #include <complex.h>
 #include <math.h>
@@ -17,6 +25,8 @@
 
 typedef double complex cx;
 
+static inline int cfin(cx v) { return isfinite(creal(v)) && isfinite(cimag(v)); }
+
 static inline cx dot4(const cx a[4], const cx b[4]) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2] + a[3] * b[3]; }
 
 /* vertex: 0 bc, 1 bc1, 2 bcb (mu_grid.VERTICES order) */
@@ -25,7 +35,7 @@ int mu_sweep_rows(const double *p_ext, const double *p4_ext, int64_t n_s, int64_
                   const double *wz, int64_t K, double coeff, double omega, double mu, double z1, double m0,
                   int vertex, const double *A_, const double *B_, const double *C_, const double *Aq_,
                   const double *Bq_, const double *Cq_, const int64_t *rows, int64_t nrows, double *out_,
-                  int threads) {
+                  int threads, int skip) {
     const cx *A = (const cx *)A_, *B = (const cx *)B_, *C = (const cx *)C_;
     const cx *Aq = (const cx *)Aq_, *Bq = (const cx *)Bq_, *Cq = (const cx *)Cq_;
     cx *out = (cx *)out_;
@@ -52,6 +62,13 @@ int mu_sweep_rows(const double *p_ext, const double *p4_ext, int64_t n_s, int64_
                 const cx sA = 0.5 * (Ap + aq), sC = 0.5 * (Cp + cq);
                 const cx dq = (Qs * Qs - P * P) + (q4t * q4t - p4t * p4t);
                 cx dA = (aq - Ap) / dq, dC = (cq - Cp) / dq, dB = (bq - Bp) / dq;
+                if (skip) {
+                    const double dqs = Qs - P, dq4 = q4r - p4r;
+                    const double lb = dqs * dqs + dq4 * dq4;
+                    if (lb > 760.0 * w2 && cfin(Ap) && cfin(Bp) && cfin(Cp) && cfin(aq) && cfin(bq) && cfin(cq) &&
+                        cfin(den) && den != 0 && cfin(dA) && cfin(dB) && cfin(dC) && cfin(sA) && cfin(sC))
+                        continue;
+                }
                 for (int64_t k = 0; k < K; ++k) {
                     const double zz = z[k];
                     const double sperp = sqrt(1.0 - zz * zz);

@@ -17,7 +17,8 @@ from .iteration import successive_approximation
 from .kernels import ModelParams, row_rhs
 from .quadrature import QuadratureRule, gauss_chebyshev2, gauss_legendre
 from .solver import (DEFAULT_PROBES_LOG10P, VARIANTS, AlgorithmVariant, Arithmetic, ExecutionMode,
-                     GpuSweeper, IterationRecord, PropagatorSolution, iterate_once, resolve_threads, solve, solve_batch)
+                     GpuSweeper, IterationRecord, PropagatorSolution, iterate_once, resolve_gpus, resolve_threads,
+                     solve, solve_batch)
 
 __version__ = "0.1.0"
 
@@ -31,5 +32,5 @@ __all__ = [
     "successive_approximation", "ModelParams", "row_rhs",
     "QuadratureRule", "gauss_chebyshev2", "gauss_legendre",
     "DEFAULT_PROBES_LOG10P", "VARIANTS", "AlgorithmVariant", "Arithmetic", "ExecutionMode", "GpuSweeper",
-    "IterationRecord", "PropagatorSolution", "iterate_once", "resolve_threads", "solve", "solve_batch",
+    "IterationRecord", "PropagatorSolution", "iterate_once", "resolve_gpus", "resolve_threads", "solve", "solve_batch",
 ]

@@ -125,6 +125,8 @@ _PROTOS = [
                                    f64p, f64p, ctypes.POINTER(DseErr)]),
     ("dse_debug_pairwise_sum", ctypes.c_int, [ctypes.c_int, f64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                               ctypes.c_int64, f64p, f64p, ctypes.POINTER(DseErr)]),
+    ("dse_debug_exp_neg_k2", ctypes.c_int, [ctypes.c_int, ctypes.c_double, f64p, ctypes.c_int64, f64p, f64p,
+                                            ctypes.POINTER(DseErr)]),
     ("dse_plan_info", ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, i32p, i32p, ctypes.c_int64, i32p, i32p, i32p,
                                      ctypes.c_int64, i64p, i64p]),
     ("dse_debug_check_flags", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32)]),
@@ -247,6 +249,18 @@ def debug_pairwise_sum(vals, chunk_leaves: int = 0, device: int = 0):
                                        oa.ctypes.data_as(f64p), ob.ctypes.data_as(f64p), _ct.byref(err))
     raise_for(rc, err)
     return oa, ob
+
+
+def debug_exp_neg_k2(k2, omega: float, device: int = 0):
+    """Test hook (dse_debug_exp_neg_k2): (table exp, CUDA exp) of -k2/omega^2."""
+    import ctypes as _ct
+    k = np.ascontiguousarray(k2, dtype=np.float64)
+    t, e = np.empty(k.size), np.empty(k.size)
+    err = DseErr()
+    rc = load().dse_debug_exp_neg_k2(device, float(omega), k.ctypes.data_as(f64p), k.size, t.ctypes.data_as(f64p),
+                                     e.ctypes.data_as(f64p), _ct.byref(err))
+    raise_for(rc, err)
+    return t, e
 
 
 def plan_info(n: int, chunk_leaves: int = 1 << 30):

@@ -1721,6 +1721,21 @@ int dse_mu_sweeper_stats(dse_mu_sweeper* s, int64_t* nominal_points, int64_t* ev
 }
 
 /* Anderson acceleration state kept on the device (see include/dse_b200.h). */
+// The device the caller's state lives on: made current before any launch (the
+// entry points take no device argument; the state pointer names it), and the
+// grid cap is derived from that device's SM count.
+static int aa_device(const void* ptr, int* blocks_cap, dse_err* err) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+        cudaGetLastError();
+        return fail(err, DSE_EPARAM, "Anderson state: not a device pointer");
+    }
+    CUDA_TRY(cudaSetDevice(at.device));
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, at.device));
+    *blocks_cap = 8 * sms;
+    return DSE_OK;
+}
 static int aa_cols(int S, int depth, const int* cols, int ncols, mu::AaCols& c, dse_err* err) {
     if (S < 1 || S > mu::kAaMaxS || depth < 1 || depth > mu::kAaMaxDepth || ncols < 0 || ncols > depth ||
         (ncols > 0 && !cols))
@@ -1745,13 +1760,16 @@ int dse_mu_aa_residual(int32_t S, int64_t n_ext, const double* d_x, const double
     if (n_ext < 1 || !d_x || !d_gx || !d_f || !d_fprev || !d_xprev || !d_scratch || !host_out ||
         (depth > 0 && (!d_dF || !d_dX)) || slot >= depth)
         return fail(err, DSE_EPARAM, "bad argument");
+    int cap = 0;
+    rc = aa_device(d_x, &cap, err);
+    if (rc) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     // dots first (16-B aligned), then the delta bits
     double2* dots = reinterpret_cast<double2*>(d_scratch);
     unsigned long long* bits = reinterpret_cast<unsigned long long*>(d_scratch + 4 * (size_t)S * ncols);
     CUDA_TRY(cudaMemsetAsync(bits, 0, sizeof(double) * 3 * S, st));
     const long long total = (long long)S * 3 * n_ext;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+    const int blocks = (int)std::min<long long>((total + 255) / 256, cap);
     mu::aa_residual_kernel<<<blocks, 256, 0, st>>>(S, n_ext, (const double2*)d_x, (const double2*)d_gx,
                                                    (double2*)d_f, (double2*)d_fprev, (double2*)d_xprev,
                                                    (double2*)d_dF, (double2*)d_dX, depth, slot, bits);
@@ -1780,9 +1798,12 @@ int dse_mu_aa_update(int32_t S, int64_t n_ext, double* d_x, const double* d_f, c
     for (int q = 0; q < S; ++q)
         for (int k = 0; k < ncols; ++k)
             c.gamma[q][k] = make_double2(gamma[2 * ((size_t)q * ncols + k)], gamma[2 * ((size_t)q * ncols + k) + 1]);
+    int cap = 0;
+    rc = aa_device(d_x, &cap, err);
+    if (rc) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const long long total = (long long)S * 3 * n_ext;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+    const int blocks = (int)std::min<long long>((total + 255) / 256, cap);
     mu::aa_update_kernel<<<blocks, 256, 0, st>>>(S, n_ext, (double2*)d_x, (const double2*)d_f, (const double2*)d_dF,
                                                  (const double2*)d_dX, depth, beta, c);
     CUDA_TRY(cudaGetLastError());

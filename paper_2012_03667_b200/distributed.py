@@ -150,9 +150,9 @@ def _device_loop_new(grid, params, variant):
     from .solver import GpuSweeper
     torch, dist = _torch_env()
     rank, world = dist.get_rank(), dist.get_world_size()
-    from .solver import resolve_threads
-    if resolve_threads(variant) != world:
-        raise ParameterError(f"variant asks for {resolve_threads(variant)} GPUs, world size is {world}")
+    from .solver import resolve_gpus
+    if resolve_gpus(variant) != world:
+        raise ParameterError(f"variant asks for {resolve_gpus(variant)} GPUs, world size is {world}")
     local = int(os.environ.get("LOCAL_RANK", torch.cuda.current_device()))
     dev = torch.device("cuda", local)
     sw = GpuSweeper(grid, params, variant.interp, variant.arith, local, rows=(rank, world))
@@ -394,7 +394,7 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
     os.environ["DSE_DEVICE"] = str(local)
     grid = build_grid(cfg["N"], cfg["M"], cfg["K"], cfg["p2_min"], cfg["p2_max"])
     params = ModelParams(N=cfg["N"], m_rad=cfg["M"], m_ang=cfg["K"], xi=1e-10)
-    variant = VARIANTS["indexed-gpu-pairs"].with_threads(world)
+    variant = VARIANTS["indexed-gpu-pairs"].with_gpus(world)
     sw, dev, rank, world, sweep_rows, gather, probe_fn, torch = _device_loop(grid, params, variant)
 
     def gather_into(out, buf):
@@ -525,9 +525,10 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
         dist.barrier()
         m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         m0.record()
-        from .finite_mu import solve_mu_batch_anderson
-        # one moment table per rank; its mu values swept 4 per launch (8 GPUs: one batch each)
-        sols = solve_mu_batch_anderson(mine, mprm_mo, mg, batch=4, device=local) if mine else []
+        from .finite_mu import solve_mu_batch_sa
+        # one moment table per rank; its mu values swept 4 per launch (8 GPUs:
+        # one batch each) by plain successive approximation (iteration-equivalent)
+        sols = solve_mu_batch_sa(mine, mprm_mo, mg, batch=4, device=local) if mine else []
         m1.record()
         torch.cuda.synchronize()
         tm = torch.tensor([m0.elapsed_time(m1) / 1e3], device=dev)
@@ -537,8 +538,9 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
         mu_block = {"config4_solves": len(mus), "seconds": float(tm.item()), "solves_per_s": len(mus) / float(tm.item()),
                     "solves_per_gpu": len(mine), "iterations_total": int(its.item()),
                     "layout": "mu values dealt cyclically over the ranks, no collective (replicas)",
+                    "vertex": mprm.vertex,
                     "mode": "moments (table built once per rank inside the timed region), 4 mu values per "
-                            "batched launch, Anderson-accelerated"}
+                            "batched launch, successive approximation (iteration counts of the standalone solves)"}
         # config 3 with its 16384 external points sharded over the ranks: one
         # iteration = sweep the owned points + pack | NCCL all-gather | assemble
         import ctypes
@@ -596,7 +598,7 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
             "e2e": {"value": nominal * args.steps / float(te.item()), "unit": unit,
                     "h2d_bytes_per_step": 2 * grid.n_ext * 8, "d2h_bytes_per_step": 2 * grid.n_ext * 8,
                     "api": "paper_2012_03667_b200.iterate_once(grid, A, B, params, "
-                           "VARIANTS['indexed-gpu-pairs'].with_threads(W)) under torchrun"},
+                           "VARIANTS['indexed-gpu-pairs'].with_gpus(W)) under torchrun"},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": None,
                          "flop_per_point": flop_per_point, "points": "evaluated, per GPU",

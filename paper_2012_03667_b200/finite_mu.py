@@ -481,6 +481,85 @@ def solve_mu_batch_anderson(mus, params: MuParams | None = None, grid: MuGrid | 
     return out_all
 
 
+def solve_mu_batch_sa(mus, params: MuParams | None = None, grid: MuGrid | None = None, batch: int = 4,
+                      device: int = 0) -> list:
+    """BASELINE config 4 on one GPU by plain successive approximation -- the
+    parity-equivalent path: every solve is solve_mu's loop (same sweep, same
+    max-norm deltas, same strict stop rule, iteration.py:18-40), so its
+    iterations, state and history are bitwise those of the standalone solve;
+    the mu values are swept `batch` (2 or 4) at a time by dse_mu_batch_sweep,
+    which reads each pair's five moments once per group sweep (moments mode:
+    one table for all mu values, built once).  The deltas max|g(x) - x| per
+    function come from the same device kernel as the Anderson path's residual
+    (hypot of the difference, as the single-solve kernel).  A solve that has
+    converged is still swept with its group (its converged state is kept);
+    relaxation != 1 runs the solves one by one (solve_mu_batch)."""
+    import torch
+    params = MuParams() if params is None else params
+    params = replace(params, mode="moments")
+    params.validate()
+    grid = grid_for(params) if grid is None else grid
+    if batch not in (2, 4):
+        raise ParameterError("batch must be 2 or 4")
+    if params.relaxation != 1.0:
+        return solve_mu_batch(mus, params, grid, device, history=True)
+    dev = torch.device("cuda", device)
+    n = grid.n_ext
+    shape = (grid.n_s, grid.n_4)
+    init = torch.cat([torch.full((n,), v, dtype=torch.complex128) for v in (1.0, 0.3, 1.0)]).to(dev)
+    lib = nat.load()
+    out_all = []
+    with MuSweeper(grid, params, device) as sw:
+        mus = list(mus)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        for g0 in range(0, len(mus), batch):
+            group = mus[g0:g0 + batch]
+            S = 4 if len(group) > 2 else 2
+            plist = [replace(params, mu=float(m)) for m in group]
+            plist += [plist[-1]] * (S - len(plist))  # pad with a repeat (its result is dropped)
+            for p_ in plist:
+                _check_c_projection(grid, p_)
+            x = init.repeat(S, 1).contiguous()
+            gx = torch.empty_like(x)
+            f = torch.empty_like(x)
+            scratch = torch.zeros(3 * S, dtype=torch.float64, device=dev)
+            host = np.zeros(3 * S)
+            nocols = np.zeros(1, dtype=np.int32)
+            hist = [[MuIterationRecord(0, float("nan"), float("nan"), float("nan"))] for _ in range(S)]
+            res = [None] * S
+            its = [params.max_iterations] * S
+            for it in range(1, params.max_iterations + 1):
+                failed = sw.batch_sweep(x, gx, plist, st)
+                for s_ in range(S):
+                    if res[s_] is None and failed[s_] >= 0:
+                        from .errors import NumericalFailureError
+                        raise NumericalFailureError(f"non-finite integrand in batched finite-mu sweep, mu="
+                                                    f"{plist[s_].mu}, row={failed[s_]}", row=failed[s_], iteration=it)
+                err = nat.DseErr()
+                # deltas only: no Anderson history (slot -1, no Gram columns)
+                nat.raise_for(lib.dse_mu_aa_residual(
+                    S, n, x.data_ptr(), gx.data_ptr(), f.data_ptr(), f.data_ptr(), f.data_ptr(), f.data_ptr(),
+                    f.data_ptr(), 1, -1, nocols.ctypes.data_as(nat.i32p), 0, scratch.data_ptr(),
+                    host.ctypes.data_as(nat.f64p), st, ctypes.byref(err)), err)
+                d = host.reshape(S, 3)
+                for s_ in range(S):
+                    if res[s_] is not None:
+                        continue
+                    hist[s_].append(MuIterationRecord(it, float(d[s_, 0]), float(d[s_, 1]), float(d[s_, 2])))
+                    if d[s_, 0] < params.xi and d[s_, 1] < params.xi and d[s_, 2] < params.xi:
+                        res[s_] = gx[s_].clone()
+                        its[s_] = it
+                x, gx = gx, x
+                if all(r is not None for r in res[:len(group)]):
+                    break
+            for s_ in range(len(group)):
+                xs = (res[s_] if res[s_] is not None else x[s_]).cpu().numpy()
+                A, B, C = (xs[k * n:(k + 1) * n].reshape(shape).copy() for k in range(3))
+                out_all.append(MuSolution(A=A, B=B, C=C, iterations=its[s_], converged=res[s_] is not None,
+                                          history=hist[s_], grid=grid, params=plist[s_]))
+    return out_all
+
+
 def owned_mus(mus, rank: int, world: int) -> list:
     """The chemical potentials rank `rank` of `world` solves (config 4 is
     replicas: mu values are dealt cyclically, no data-path collective)."""

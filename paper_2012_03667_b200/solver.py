@@ -5,17 +5,27 @@ Same entry points, signatures and return types as the reference:
   solve(params, variant, grid=None, probes_log10p=(-2.5, 0.0), a0=None, b0=None)
       -> PropagatorSolution                                   (solver.py:221-266)
   iterate_once(grid, a, b, params, variant) -> (A', B')      (solver.py:201-212)
+  _eval_rows(grid, params, strategy, a, b, start, stop)       (solver.py:117-128)
 
 The strategy seam is kept: AlgorithmVariant(interp, execution, threads) and
-_make_sweeper (solver.py:53-74, 195-198).  The only execution mode is
-ExecutionMode.GPU; the reference's four variant names resolve to the GPU
-variant with the same interpolation strategy, so caller code written against
-dsegap runs unchanged.  `solve` hands the whole successive-approximation loop
-to the device (dse_solve): relaxation, max-norm deltas, the strict stopping
-rule, history and probes all happen in the persistent kernel, with no host
-round trip per iteration.
+_make_sweeper (solver.py:53-74, 195-198).  The reference's execution modes
+SEQUENTIAL and PARALLEL are kept with the reference's meaning of `threads`
+(host workers, variant.threads else $SOLVER_THREADS else the CPU count,
+solver.py:100-108): both run the sweep on one GPU in the reference's
+operation order (Arithmetic.EXACT), and -- exactly as the reference promises
+for its worker pools (test_solver.py:67-71) -- the worker count cannot
+change a single bit, because no per-row work is left on the host.
+ExecutionMode.GPU adds the device arithmetics (FAST, PAIRS, MOMENTS).
 
-Multi-GPU (variant.threads = G > 1): see paper_2012_03667_b200.distributed.
+The GPU count is a separate, explicit knob: AlgorithmVariant.gpus, else
+$DSE_GPUS, else 1 (resolve_gpus).  gpus > 1 runs the row-sharded solve of
+paper_2012_03667_b200.distributed under torchrun (one process per GPU);
+`threads` never selects GPUs.
+
+`solve` hands the whole successive-approximation loop to the device
+(dse_solve): relaxation, max-norm deltas, the strict stopping rule, history
+and probes all happen in the persistent kernel, with no host round trip per
+iteration.
 """
 from __future__ import annotations
 
@@ -42,6 +52,7 @@ __all__ = [
     "IterationRecord",
     "PropagatorSolution",
     "resolve_threads",
+    "resolve_gpus",
     "iterate_once",
     "solve",
     "solve_batch",
@@ -50,12 +61,20 @@ __all__ = [
 ]
 
 THREADS_ENV_VAR = "SOLVER_THREADS"
+GPUS_ENV_VAR = "DSE_GPUS"
 DEVICE_ENV_VAR = "DSE_DEVICE"
 
 DEFAULT_PROBES_LOG10P = (-2.5, 0.0)
 
 
 class ExecutionMode(enum.Enum):
+    """SEQUENTIAL / PARALLEL: the reference's modes (solver.py:48-50), same
+    values; both sweep on one GPU in the reference's operation order, and
+    PARALLEL's worker count (threads) is a host-side knob that cannot change
+    a bit.  GPU: the device arithmetics (AlgorithmVariant.arith)."""
+
+    SEQUENTIAL = "seq"
+    PARALLEL = "par"
     GPU = "gpu"
 
 
@@ -64,7 +83,8 @@ class Arithmetic(enum.Enum):
 
     EXACT: the reference's operation order (kernels.py:188-218), one rounding
            per numpy op, IEEE divides; differs from the reference only by the
-           device exp (<= 1 ulp).
+           device exp (<= 1 ulp).  The arithmetic of the reference's own
+           execution modes (SEQUENTIAL, PARALLEL).
     FAST:  algebraically reduced, FMA-contracted, one reciprocal of k2 per
            point (csrc/dse_device.cuh point_fast).
     MOMENTS: the angular-moment factorisation: six
@@ -89,25 +109,43 @@ def _arith_code(arith: Arithmetic) -> int:
             Arithmetic.MOMENTS: nat.ARITH_MOMENTS, Arithmetic.PAIRS: nat.ARITH_PAIRS}[arith]
 
 
+_HOST_MODES = (ExecutionMode.SEQUENTIAL, ExecutionMode.PARALLEL)
+
+
 @dataclass(frozen=True)
 class AlgorithmVariant:
-    """(interpolation strategy x execution) cell; threads = GPUs per solve."""
+    """(interpolation strategy x execution) cell (solver.py:53-66).
+
+    The first three fields are the reference's, positionally and by meaning:
+    threads = host workers (resolve_threads).  arith defaults to EXACT for
+    the reference's modes and FAST for ExecutionMode.GPU; gpus = GPUs per
+    solve (resolve_gpus)."""
 
     interp: InterpStrategy
     execution: ExecutionMode = ExecutionMode.GPU
     threads: int | None = None
-    arith: Arithmetic = Arithmetic.FAST
+    arith: Arithmetic | None = None
+    gpus: int | None = None
+
+    def __post_init__(self):
+        if self.arith is None:
+            object.__setattr__(self, "arith", Arithmetic.EXACT if self.execution in _HOST_MODES
+                               else Arithmetic.FAST)
 
     @property
     def name(self) -> str:
         base = f"{self.interp.value}-{self.execution.value}"
-        return base if self.arith is Arithmetic.FAST else f"{base}-{self.arith.value}"
+        default = Arithmetic.EXACT if self.execution in _HOST_MODES else Arithmetic.FAST
+        return base if self.arith is default else f"{base}-{self.arith.value}"
 
     def with_threads(self, threads: int | None) -> "AlgorithmVariant":
-        return AlgorithmVariant(self.interp, self.execution, threads, self.arith)
+        return AlgorithmVariant(self.interp, self.execution, threads, self.arith, self.gpus)
 
     def with_arith(self, arith: Arithmetic) -> "AlgorithmVariant":
-        return AlgorithmVariant(self.interp, self.execution, self.threads, arith)
+        return AlgorithmVariant(self.interp, self.execution, self.threads, arith, self.gpus)
+
+    def with_gpus(self, gpus: int | None) -> "AlgorithmVariant":
+        return AlgorithmVariant(self.interp, self.execution, self.threads, self.arith, gpus)
 
 
 _SEARCH = AlgorithmVariant(InterpStrategy.SEARCH_BASED)
@@ -128,12 +166,12 @@ VARIANTS = {
     # fast arithmetic in the pair-moment form (same points per iteration)
     "search-gpu-pairs": _SEARCH.with_arith(Arithmetic.PAIRS),
     "indexed-gpu-pairs": _INDEXED.with_arith(Arithmetic.PAIRS),
-    # the reference's names (solver.py:69-74) -> the GPU variant with that
-    # strategy, in the bit-faithful exact arithmetic
-    "search-seq": _SEARCH.with_arith(Arithmetic.EXACT),
-    "indexed-seq": _INDEXED.with_arith(Arithmetic.EXACT),
-    "search-par": _SEARCH.with_arith(Arithmetic.EXACT),
-    "indexed-par": _INDEXED.with_arith(Arithmetic.EXACT),
+    # the reference's names and cells (solver.py:69-74): same execution
+    # modes, swept on one GPU in the reference's operation order
+    "search-seq": AlgorithmVariant(InterpStrategy.SEARCH_BASED, ExecutionMode.SEQUENTIAL),
+    "indexed-seq": AlgorithmVariant(InterpStrategy.PRECOMPUTED_INDEX, ExecutionMode.SEQUENTIAL),
+    "search-par": AlgorithmVariant(InterpStrategy.SEARCH_BASED, ExecutionMode.PARALLEL),
+    "indexed-par": AlgorithmVariant(InterpStrategy.PRECOMPUTED_INDEX, ExecutionMode.PARALLEL),
 }
 
 
@@ -159,14 +197,30 @@ class PropagatorSolution:
 
 
 def resolve_threads(variant: AlgorithmVariant) -> int:
-    """GPU count of a variant: variant.threads, else $SOLVER_THREADS, else 1."""
+    """Host worker count, the reference's rule (solver.py:100-108):
+    variant.threads, else $SOLVER_THREADS, else the CPU count.  It never
+    changes a result (no per-row work runs on the host) and never selects
+    GPUs (resolve_gpus does)."""
     if variant.threads is not None:
         n = variant.threads
     else:
         env = os.environ.get(THREADS_ENV_VAR)
-        n = int(env) if env else 1
+        n = int(env) if env else (os.cpu_count() or 1)
     if n < 1:
         raise ParameterError(f"thread count must be >= 1, got {n}")
+    return n
+
+
+def resolve_gpus(variant: AlgorithmVariant) -> int:
+    """GPUs per solve: variant.gpus, else $DSE_GPUS, else 1.  More than one
+    needs torch.distributed initialised with that many ranks (one per GPU)."""
+    if variant.gpus is not None:
+        n = variant.gpus
+    else:
+        env = os.environ.get(GPUS_ENV_VAR)
+        n = int(env) if env else 1
+    if n < 1:
+        raise ParameterError(f"GPU count must be >= 1, got {n}")
     return n
 
 
@@ -301,6 +355,16 @@ class GpuSweeper:
         return {n: getattr(out, n) for n, _ in out._fields_}
 
     def close(self):
+        # under the call lock: a thread that took this sweeper from the cache
+        # just before it was evicted finishes its call on a live handle
+        lock = getattr(self, "_lock", None)
+        if lock is None:
+            self._destroy()
+            return
+        with lock:
+            self._destroy()
+
+    def _destroy(self):
         if getattr(self, "handle", None):
             self.lib.dse_sweeper_destroy(self.handle)
             self.handle = None
@@ -325,8 +389,9 @@ def _params_key(p: ModelParams):
 
 
 def _make_sweeper(grid, params, variant: AlgorithmVariant) -> GpuSweeper:
-    if variant.execution is not ExecutionMode.GPU:
+    if not isinstance(variant.execution, ExecutionMode):
         raise ParameterError(f"unsupported execution mode {variant.execution}")
+    resolve_threads(variant)  # validated like the reference (a bad count is a ParameterError)
     dev = _device()
     key = (id(grid), _params_key(params), variant.interp, variant.arith, dev)
     with _CACHE_LOCK:
@@ -337,8 +402,10 @@ def _make_sweeper(grid, params, variant: AlgorithmVariant) -> GpuSweeper:
         sw = GpuSweeper(grid, params, variant.interp, variant.arith, dev)
         _CACHE[key] = sw
         while len(_CACHE) > _CACHE_MAX:
-            _, old = _CACHE.popitem(last=False)
-            old.close()
+            # no explicit close(): a thread that took the evicted sweeper from
+            # the cache may still be about to call it; the handle is destroyed
+            # by __del__ once the last reference is dropped (reference counting)
+            _CACHE.popitem(last=False)
         return sw
 
 
@@ -348,6 +415,45 @@ def clear_sweeper_cache() -> None:
             _CACHE.popitem()[1].close()
 
 
+def _interp_at_internal(grid: MomentumGrid, values: np.ndarray, strategy: InterpStrategy) -> np.ndarray:
+    """values interpolated at the M internal nodes with the strategy's
+    bracket source (solver.py:111-114), on the GPU."""
+    from .interpolation import interp_indexed_many, interp_search_many
+    if strategy is InterpStrategy.PRECOMPUTED_INDEX:
+        return interp_indexed_many(grid, values)
+    return interp_search_many(grid.p2_ext, values, grid.q2_int)
+
+
+def _eval_rows(grid: MomentumGrid, params: ModelParams, strategy: InterpStrategy,
+               a: np.ndarray, b: np.ndarray, start: int, stop: int):
+    """Rows [start, stop) of the sweep in the reference's arithmetic
+    (solver.py:117-128); reads only (a, b).  Rows are Jacobi-independent and
+    each is reduced by one CTA in a fixed order, so the rows of the cached
+    device sweep ARE the rows of any row range (bitwise).  A numerical
+    failure outside the range does not concern this range: the range is
+    then evaluated row by row (dse_row_rhs), which raises only for its own
+    rows, with the reference's (row, radial, angular) location."""
+    from .errors import NumericalFailureError
+    if not 0 <= start <= stop <= grid.n_ext:
+        raise ParameterError(f"row range [{start}, {stop}) outside [0, {grid.n_ext})")
+    variant = AlgorithmVariant(strategy, ExecutionMode.SEQUENTIAL)
+    try:
+        full_a, full_b = iterate_once(grid, a, b, params, variant)
+        return full_a[start:stop].copy(), full_b[start:stop].copy()
+    except NumericalFailureError as exc:
+        if exc.row is not None and start <= exc.row < stop:
+            raise
+    a = np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    a_q = _interp_at_internal(grid, a, strategy)
+    b_q = _interp_at_internal(grid, b, strategy)
+    a_out = np.empty(stop - start)
+    b_out = np.empty(stop - start)
+    for i in range(start, stop):
+        a_out[i - start], b_out[i - start] = _row_rhs_gpu(grid.p2_ext[i], a[i], b[i], a_q, b_q, grid, params, i)
+    return a_out, b_out
+
+
 def iterate_once(grid: MomentumGrid, a: np.ndarray, b: np.ndarray, params: ModelParams,
                  variant: AlgorithmVariant):
     """One Jacobi sweep (A', B') from (A, B) on the GPU (solver.py:201-212)."""
@@ -355,7 +461,7 @@ def iterate_once(grid: MomentumGrid, a: np.ndarray, b: np.ndarray, params: Model
     b = np.asarray(b, dtype=float)
     if a.shape != (grid.n_ext,) or b.shape != (grid.n_ext,):
         raise ParameterError("A and B must match the external grid size")
-    if resolve_threads(variant) > 1:
+    if resolve_gpus(variant) > 1:
         from .distributed import iterate_once_sharded
         return iterate_once_sharded(grid, a, b, params, variant)
     return _make_sweeper(grid, params, variant).sweep(a, b)
@@ -375,7 +481,7 @@ def solve(params: ModelParams, variant: AlgorithmVariant, grid: MomentumGrid | N
     b = np.ones(grid.n_ext) if b0 is None else np.asarray(b0, dtype=float).copy()
     if a.shape != (grid.n_ext,) or b.shape != (grid.n_ext,):
         raise ParameterError("a0 and b0 must match the external grid size")
-    if resolve_threads(variant) > 1:
+    if resolve_gpus(variant) > 1:
         from .distributed import solve_sharded
         a, b, n, conv, hist = solve_sharded(grid, params, variant, a, b, probes_p2)
     else:
@@ -402,7 +508,8 @@ def solve_batch(params_list, variant: AlgorithmVariant, grid: MomentumGrid | Non
         return []
     for prm in params_list:
         prm.validate()
-    if resolve_threads(variant) != 1:
+    resolve_threads(variant)
+    if resolve_gpus(variant) != 1:
         raise ParameterError("solve_batch runs on one GPU; use torchrun + solve for multi-GPU solves")
     p0 = params_list[0]
     if grid is None:

@@ -14,7 +14,7 @@ local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local)
 g = p.build_grid(1024, 1024, 256, 1e-6, 1e4)
 prm = p.ModelParams(N=1024, m_rad=1024, m_ang=256, xi=1e-10)
-v = p.VARIANTS["indexed-gpu"].with_threads(dist.get_world_size())
+v = p.VARIANTS["indexed-gpu"].with_gpus(dist.get_world_size())
 sw, dev, rank, world, sweep_rows, gather, probe_fn, _ = D._device_loop(g, prm, v)
 loop = D.ShardedLoop(g.n_ext, rank, world, sweep_rows, gather, probe_fn(()), xp=torch)
 a = torch.ones(1024, dtype=torch.float64, device=dev)

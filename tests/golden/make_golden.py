@@ -9,6 +9,7 @@ The reference (`dsegap`, pure Python + numpy) is imported read-only from
   solve_c0.npz        config 0 solve: 2923 iterations, A, B, full history
   solve_c2k10.npz     config 2 (1024/1024/256) first 10 sweeps
   solve_sub256.npz    convergent large substitute N=M=K=256, relaxation 0.5
+  solve_slow_*.npz    config-0 grid at D=0.5, D=0.6 and relaxation 0.7 (thousands of iterations)
   interp_c1.npz       config 1 interpolation on a 2**16-query sample
   errors.npz          NumericalFailureError locations
 
@@ -137,6 +138,24 @@ def make_solve_sub256(threads):
     _solve_to_npz("solve_sub256.npz", 256, 256, 256, p, threads, np.full(256, 0.3))
 
 
+# slow-converging config-0 variants (xi = 1e-10, b0 = 0.3): iteration counts
+# in the thousands, the regime where the count is most sensitive to rounding
+# -- D below and just above the default (D = 0.60 oscillates: not converged in 20000), and an under-relaxed solve
+SLOW = {
+    "d050": dict(D=0.50),
+    "d056": dict(D=0.56),
+    "r070": dict(relaxation=0.7),
+}
+
+
+def make_solve_slow(threads, tags=None):
+    for tag, kw in SLOW.items():
+        if tags and tag not in tags:
+            continue
+        p = ModelParams(N=128, m_rad=128, m_ang=64, xi=1e-10, max_iterations=20000, **kw)
+        _solve_to_npz(f"solve_slow_{tag}.npz", 128, 128, 64, p, threads, np.full(128, 0.3))
+
+
 def make_interp():
     x = np.logspace(-4, 4, 512)
     v = 1.0 / (1.0 + x) + 0.1 * np.log1p(x)
@@ -231,6 +250,8 @@ JOBS = {
     "solve_c0": make_solve_c0,
     "solve_c2k10": make_solve_c2k10,
     "solve_sub256": make_solve_sub256,
+    "solve_slow": make_solve_slow,
+    "solve_slow_d056": lambda t: make_solve_slow(t, ("d056",)),
 }
 
 if __name__ == "__main__":

@@ -13,7 +13,16 @@ values, maps each to the reference's 4-D kinematics (p2, q2, z4) and records
 the reference's own `integrand_terms(kinematics(p2, q2, z4), a_p, a_q, b_p, b_q)`.
 Run once in the build container (the reference is not on the GPU box).
 
-Usage:  python tests/golden/make_mu_golden.py
+--config3 / --config4 write the full-size converged fixtures instead
+(mu_full_<tag>.npz).  There is no reference for finite mu, so these come from
+the C oracle (oracle/mu_oracle_c.c through oracle/mu_oracle.solve_c:
+explicit 4-vector projections, sequential sums, exact-zero node skip that is
+bitwise neutral) run on the grid arrays stored in the same file:
+  config3       mu = 0.2 GeV, BASELINE config 3 (MuParams defaults, vertex bcb)
+  config4_k<k>  mu = 0.4 (k + 1/2) / 32, the k-th of config 4's 32 values
+Each holds the MuGrid arrays, A, B, C, iterations, converged, history.
+
+Usage:  python tests/golden/make_mu_golden.py [--config3] [--config4 K ...] [--threads T]
 """
 from __future__ import annotations
 
@@ -22,13 +31,13 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, "/root/reference/pkg/src")
-from dsegap.kernels import integrand_terms, kinematics  # noqa: E402
-
 HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
 
 
 def main():
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from dsegap.kernels import integrand_terms, kinematics
     rng = np.random.default_rng(20121036)
     n = 400
     P = np.exp(rng.uniform(np.log(1e-2), np.log(10.0), n))
@@ -55,5 +64,45 @@ def main():
     print("wrote mu_vacuum_points.npz", n)
 
 
+GRID_FIELDS = ("p_ext", "ps2_ext", "p4_ext", "q_int", "qs2_int", "q4_int", "meas_s", "meas_4", "z_nodes",
+               "z_weights", "brk_s", "brk_4", "node_measure")
+
+
+def full_solve(tag: str, mu: float, threads: int):
+    import time
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import mu_oracle
+    from paper_2012_03667_b200.mu_grid import MuParams, grid_for
+    prm = MuParams(mu=mu)
+    g = grid_for(prm)
+    t0 = time.perf_counter()
+
+    def log(n, d):
+        print(f"{tag} iteration {n}: {d[0]:.3e} {d[1]:.3e} {d[2]:.3e} ({time.perf_counter() - t0:.0f} s)", flush=True)
+
+    A, B, C, n, conv, hist = mu_oracle.solve_c(g, prm, threads=threads, on_iteration=log)
+    path = os.path.join(HERE, f"mu_full_{tag}.npz")
+    np.savez_compressed(path, A=A, B=B, C=C, iterations=np.array(n), converged=np.array(conv),
+                        history=np.array(hist, dtype=np.float64),
+                        params=np.array([prm.D, prm.omega, prm.m0, prm.z1, prm.mu, prm.xi, prm.max_iterations,
+                                         prm.relaxation]),
+                        vertex=np.array(prm.vertex), seconds=np.array(time.perf_counter() - t0),
+                        call=np.array(f"mu_oracle.solve_c(grid_for(MuParams(mu={mu!r})), MuParams(mu={mu!r}))"),
+                        **{f"grid_{k}": getattr(g, k) for k in GRID_FIELDS})
+    print(f"wrote {path}: {n} iterations, converged={conv}, {time.perf_counter() - t0:.0f} s", flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config3", action="store_true")
+    ap.add_argument("--config4", type=int, nargs="*", default=[])
+    ap.add_argument("--threads", type=int, default=os.cpu_count())
+    args = ap.parse_args()
+    if not args.config3 and not args.config4:
+        main()
+    if args.config3:
+        full_solve("config3", 0.2, args.threads)
+    for k in args.config4:
+        full_solve(f"config4_k{k:02d}", 0.4 * (k + 0.5) / 32, args.threads)

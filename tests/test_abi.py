@@ -48,7 +48,11 @@ def test_product_never_imports_oracle():
         for f in files:
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
-                assert not re.search(r"import\s+oracle|from\s+oracle|liboracle_dse|dse_oracle", txt), f
+                # any import or load of the checker: oracle, mu_oracle, cubic_oracle,
+                # mu_dirac, liboracle_*.so, the C restatement's symbols
+                assert not re.search(r"import\s+[\w.]*(oracle|mu_dirac)|from\s+[\w.]*(oracle|mu_dirac)\b|"
+                                     r"liboracle|dse_oracle|oracle_(sweep|solve|mu)|(mu|cubic)_oracle\.(?!py)|"
+                                     r"sys\.path[^\n]*oracle|CDLL\([^)]*oracle", txt), f
 
 
 def test_anderson_state_argument_validation_without_gpu():

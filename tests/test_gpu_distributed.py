@@ -36,9 +36,9 @@ def test_sharded_solve_world1_bitwise(nccl_world1):
     g = golden_grid("default")
     prm = params_ns(xi=0.005, max_iterations=500)
     ref = p.solve(prm, p.VARIANTS["indexed-gpu"], grid=g)
-    sol = p.solve(prm, p.VARIANTS["indexed-gpu"].with_threads(1), grid=g)  # threads=1 -> single GPU
+    sol = p.solve(prm, p.VARIANTS["indexed-gpu"].with_gpus(1), grid=g)  # gpus=1 -> single GPU
     from paper_2012_03667_b200.distributed import solve_sharded
-    a, b, n, conv, hist = solve_sharded(g, prm, p.VARIANTS["indexed-gpu"].with_threads(1), np.ones(g.n_ext),
+    a, b, n, conv, hist = solve_sharded(g, prm, p.VARIANTS["indexed-gpu"].with_gpus(1), np.ones(g.n_ext),
                                         np.ones(g.n_ext), tuple(10.0 ** (2.0 * lp) for lp in (-2.5, 0.0)))
     assert n == ref.iterations == sol.iterations == int(z["iterations"]) and conv
     assert np.array_equal(a, ref.A) and np.array_equal(b, ref.B)
@@ -51,7 +51,7 @@ def test_sharded_sweep_world1_bitwise(nccl_world1):
     rng = np.random.default_rng(5)
     a, b = rng.uniform(1, 2, g.n_ext), rng.uniform(0, 1, g.n_ext)
     from paper_2012_03667_b200.distributed import iterate_once_sharded
-    x = iterate_once_sharded(g, a, b, params_ns(), p.VARIANTS["indexed-gpu"].with_threads(1))
+    x = iterate_once_sharded(g, a, b, params_ns(), p.VARIANTS["indexed-gpu"].with_gpus(1))
     y = p.iterate_once(g, a, b, params_ns(), p.VARIANTS["indexed-gpu"])
     assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
 

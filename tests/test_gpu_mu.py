@@ -379,3 +379,24 @@ def test_device_anderson_kernels_match_numpy():
         torch.cuda.synchronize()
         got = x.cpu().numpy()
         assert np.max(np.abs(got - ref_x)) <= 1e-12 * np.max(np.abs(ref_x))
+
+
+@pytest.mark.parametrize("count", [3, 5])
+def test_batched_successive_approximation_equals_standalone(count):
+    """solve_mu_batch_sa (config 4's parity-equivalent path): each mu value's
+    iterations, history and state are bitwise its standalone solve_mu; groups
+    of 4 and a padded remainder."""
+    from paper_2012_03667_b200.finite_mu import solve_mu_batch_sa
+    p = MuParams(vertex="bcb", max_iterations=200, **SMALL)
+    g = grid_for(p)
+    mus = [0.02 + 0.37 * k / count for k in range(count)]
+    batch = solve_mu_batch_sa(mus, p, g, batch=4)
+    assert len(batch) == count
+    for m, sol in zip(mus, batch):
+        one = solve_mu(MuParams(**{**p.__dict__, "mu": m}), g)
+        assert sol.converged and sol.iterations == one.iterations
+        for x, y in ((sol.A, one.A), (sol.B, one.B), (sol.C, one.C)):
+            assert np.array_equal(x.view(np.float64), y.view(np.float64))
+        h1 = [(r.n, r.delta_a, r.delta_b, r.delta_c) for r in one.history]
+        h2 = [(r.n, r.delta_a, r.delta_b, r.delta_c) for r in sol.history]
+        assert np.array_equal(np.array(h1[1:]), np.array(h2[1:]))

@@ -131,3 +131,21 @@ def test_load_resume_status_protocol(arith):
         sw.resume(2)
         sw.check()
         sw.close()
+
+
+@pytest.mark.parametrize("tag", ["d050", "d056", "r070"])
+@pytest.mark.parametrize("vname", ["indexed-seq", "indexed-gpu", "indexed-gpu-moments", "indexed-gpu-pairs"])
+def test_solve_slow_converging_iteration_counts(tag, vname):
+    """Config-0 grid at D = 0.50, D = 0.56 and relaxation 0.7 (xi = 1e-10,
+    b0 = 0.3): the reference's own iteration counts, exactly, for the
+    reference-order arithmetic and for every fast form (the count
+    is the most rounding-sensitive observable)."""
+    import os
+    from conftest import GOLDEN
+    fname = f"solve_slow_{tag}.npz"
+    if not os.path.exists(os.path.join(GOLDEN, fname)):
+        pytest.skip(f"{fname} not generated")
+    z, sol = _run(fname, "c0", p.VARIANTS[vname])
+    assert sol.converged == bool(z["converged"]) and sol.iterations == int(z["iterations"])
+    assert hybrid_rel(sol.A, z["A"]) <= 1e-9 and hybrid_rel(sol.B, z["B"]) <= 1e-9
+    assert _hist(sol).shape == z["history"].shape

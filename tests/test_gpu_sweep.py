@@ -3,7 +3,7 @@
 Oracle: golden vectors from the reference itself (tests/golden/sweeps.npz)
 and the C restatement (oracle/).  Tolerances (SURVEY.md §8c hybrid measure):
   exact arithmetic : <= 1e-13 (only the device exp differs, <= 1 ulp)
-  fast arithmetic  : <= 1e-12
+  fast, pairs, moments : <= 2e-13 (measured <= 7.8e-14; SURVEY F7 safe budget ~1e-14 systematic)
 The reference's own bound for iterate_once vs its brute oracle is 1e-11
 (test_solver.py:83-91).
 """
@@ -16,7 +16,7 @@ from conftest import golden, golden_grid, hybrid_rel, params_ns
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"exact": 1e-13, "fast": 1e-12, "moments": 1e-12, "pairs": 1e-12}
+TOL = {"exact": 1e-13, "fast": 2e-13, "moments": 2e-13, "pairs": 2e-13}
 VAR = {"exact": p.VARIANTS["indexed-gpu-exact"], "fast": p.VARIANTS["indexed-gpu"],
        "moments": p.VARIANTS["indexed-gpu-moments"], "pairs": p.VARIANTS["indexed-gpu-pairs"]}
 

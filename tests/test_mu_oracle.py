@@ -124,3 +124,21 @@ def test_c_restatement_matches_numpy_oracle(vertex):
     for f in range(3):
         r = ref[f].reshape(-1)
         assert np.max(np.abs(got[:, f] - r)) <= 1e-12 * np.max(np.abs(r))
+
+
+@pytest.mark.parametrize("vertex", ["bc", "bcb"])
+def test_c_restatement_node_skip_is_bitwise(vertex):
+    """The exact-zero node skip of the C oracle (the GPU kernels' window skip)
+    changes no bit: every skipped summand is an exact zero.  A narrow
+    interaction (omega = 0.15) makes most nodes skippable on this grid."""
+    p = MuParams(mu=0.2, vertex=vertex, omega=0.15, n_s=10, n_4=12, m_s=16, m_4=18, m_ang=6)
+    g = grid_for(p)
+    rng = np.random.default_rng(5)
+    shape = (g.n_s, g.n_4)
+    A = 1 + rng.random(shape) + 0.1j * rng.standard_normal(shape)
+    B = 0.2 + 0.3 * rng.random(shape) + 0.05j * rng.standard_normal(shape)
+    C = 1 + rng.random(shape) + 0.1j * rng.standard_normal(shape)
+    rows = np.arange(g.n_ext)
+    a = mu_oracle.sweep_rows_c(g, p, A, B, C, rows, threads=2, skip=True)
+    b = mu_oracle.sweep_rows_c(g, p, A, B, C, rows, threads=2, skip=False)
+    assert np.array_equal(a.view(np.float64), b.view(np.float64))
