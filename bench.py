@@ -125,6 +125,34 @@ def cpu_port_rate(grid, params, budget_s: float, threads: int):
     return pts / dt, {"rows": int(picked.size), "points": int(pts), "seconds": dt}
 
 
+def table1_cpu_runners(threads=None):
+    """The CPU rows of the Table-1 harness (paper_2012_03667_b200.harness;
+    the CLI's `bench` loads them from here): the reference's four algorithms
+    (VARIANT_ORDER of reference bench.py:24) on the host,
+    as the C restatement of the reference's solve (oracle/dse_oracle.c),
+    with the reference's per-row interpolation cost (solver.py:123-125):
+    search / indexed interpolation x 1 thread / all host threads.  This is
+    bench.py's baseline leg; the package never runs a CPU sweep itself."""
+    import types
+
+    from paper_2012_03667_b200.harness import Runner
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    oracle.set_per_row_interp(True)
+    par = int(threads) if threads else oracle.max_threads()
+
+    def runner(strategy, nthreads):
+        def run(params, grid):
+            a, b, n, conv, _ = oracle.solve(grid, params, np.ones(grid.n_ext), np.ones(grid.n_ext),
+                                            probes_p2=(10.0 ** -5, 1.0), strategy=strategy, threads=nthreads)
+            return types.SimpleNamespace(A=a, B=b, iterations=n, converged=conv)
+        return run
+    return [Runner("search-cpu-seq", "cpu-port", runner(0, 1), 1),
+            Runner("indexed-cpu-seq", "cpu-port", runner(1, 1), 1),
+            Runner("search-cpu-par", "cpu-port", runner(0, par), par),
+            Runner("indexed-cpu-par", "cpu-port", runner(1, par), par)]
+
+
 def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:

@@ -68,6 +68,7 @@ def lib():
                                    _f64p, ctypes.c_int64, _f64p, _f64p, _i64p,
                                    ctypes.POINTER(ctypes.c_int), _f64p, ctypes.c_int, _i64p]
         L.oracle_max_threads.restype = ctypes.c_int
+        L.oracle_set_per_row_interp.argtypes = [ctypes.c_int]
         _LIB = L
     return _LIB
 
@@ -157,6 +158,12 @@ def sweep(grid, a, b, params, strategy: int = 1, threads: int = 1, rows=None):
         raise OracleError(f"non-finite integrand at row={err[0]}, radial={err[1]}, angular={err[2]}",
                           tuple(int(e) for e in err))
     return ao, bo
+
+
+def set_per_row_interp(on: bool) -> None:
+    """Interpolate A, B at the internal nodes once per ROW, as the reference's
+    _eval_rows does (solver.py:123-125; same bits, the reference's cost)."""
+    lib().oracle_set_per_row_interp(int(bool(on)))
 
 
 def solve(grid, params, a0, b0, probes_p2=(), strategy: int = 1, threads: int = 1):

@@ -72,3 +72,41 @@ def test_no_gpu_is_a_runtime_failure(tmp_path, gpu_available, capsys):
     rc = cli.main(["solve", "--N", "8", "--M-rad", "8", "--M-ang", "4", "--out", str(tmp_path / "s.csv"),
                    "--history", str(tmp_path / "h.csv")])
     assert rc == 1 and "error:" in capsys.readouterr().err
+
+
+def test_harness_rows_gate_and_table_without_gpu():
+    """The Table-1 harness on CPU rows only (the reference's algorithms from
+    bench.py's baseline leg, C restatement): one iteration count, agreement,
+    table and JSON schema (reference bench.py:28-50)."""
+    import bench
+    from paper_2012_03667_b200 import harness
+    prm = p.ModelParams(N=24, m_rad=20, m_ang=8)
+    rep = harness.run_bench(prm, order=(), baselines=bench.table1_cpu_runners(2))
+    assert [r.variant for r in rep.rows] == ["search-cpu-seq", "indexed-cpu-seq", "search-cpu-par",
+                                             "indexed-cpu-par"]
+    assert len({r.iterations for r in rep.rows}) == 1 and all(r.converged for r in rep.rows)
+    d = json.loads(rep.to_json())
+    assert set(d) == {"rows", "speedups", "environment"}
+    assert {"variant", "wall_s", "cpu_percent", "iterations", "converged"} <= set(d["rows"][0])
+    assert "search-cpu-seq/indexed-cpu-par" in rep.speedups
+    table = harness.format_table(rep)
+    assert table.splitlines()[0].split()[:2] == ["variant", "backend"]
+
+
+def test_harness_agreement_gate_fires_without_gpu():
+    import types
+    from paper_2012_03667_b200 import harness
+    one = types.SimpleNamespace(A=np.ones(4), B=np.zeros(4), iterations=7, converged=True)
+    off = types.SimpleNamespace(A=np.ones(4) + 1e-9, B=np.zeros(4), iterations=7, converged=True)
+    slow = types.SimpleNamespace(A=np.ones(4), B=np.zeros(4), iterations=8, converged=True)
+    mk = lambda name, sol: harness.Runner(name, "cpu-port", lambda prm, g: sol)  # noqa: E731
+    prm = p.ModelParams(N=8, m_rad=6, m_ang=2)
+    harness.run_bench(prm, order=(), baselines=[mk("a", one), mk("b", one)])
+    with pytest.raises(p.ConsistencyError):
+        harness.run_bench(prm, order=(), baselines=[mk("a", one), mk("b", off)])
+    with pytest.raises(p.ConsistencyError):
+        harness.run_bench(prm, order=(), baselines=[mk("a", one), mk("b", slow)])
+
+
+def test_cpu_rows_flag_validation(capsys):
+    assert cli.main(["bench", "--cpu-rows", "maybe"]) == 2

@@ -26,13 +26,24 @@ def test_solve_cli_default_config_and_bytes(tmp_path):
     assert len(hist) == int(z["iterations"]) + 2
 
 
-def test_bench_cli_and_agreement(tmp_path, capsys):
+def test_bench_cli_table1_rows_and_agreement(tmp_path, capsys):
+    """`bench`: the reference's four CPU algorithms (bench.py's baseline leg)
+    beside the four GPU rows, one iteration count, GPU-over-CPU speedups."""
     out = tmp_path / "b.json"
     assert cli.main(["bench", "--N", "48", "--M-rad", "40", "--M-ang", "16", "--out", str(out)]) == 0
     rep = json.loads(out.read_text())
-    assert [r["variant"] for r in rep["rows"]] == list(harness.VARIANT_ORDER)
+    names = [r["variant"] for r in rep["rows"]]
+    assert names == ["search-cpu-seq", "indexed-cpu-seq", "search-cpu-par", "indexed-cpu-par",
+                     *harness.GPU_ROWS]
+    assert [r["backend"] for r in rep["rows"]] == ["cpu-port"] * 4 + ["gpu"] * 4
     assert len({r["iterations"] for r in rep["rows"]}) == 1
-    assert "speedup search-gpu-exact/indexed-gpu" in capsys.readouterr().out
+    text = capsys.readouterr().out
+    assert "speedup search-cpu-seq/indexed-gpu-pairs" in text
+    assert any(k.startswith(("indexed-cpu-par/", "search-cpu-par/", "indexed-cpu-seq/", "search-cpu-seq/"))
+               and k.endswith("/indexed-gpu") for k in rep["speedups"])
+    assert cli.main(["bench", "--N", "48", "--M-rad", "40", "--M-ang", "16", "--cpu-rows", "off",
+                     "--out", str(out)]) == 0
+    assert [r["variant"] for r in json.loads(out.read_text())["rows"]] == list(harness.GPU_ROWS)
 
 
 def test_agreement_gate_fires(monkeypatch):
