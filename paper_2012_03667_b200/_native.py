@@ -125,6 +125,11 @@ _PROTOS = [
                                    f64p, f64p, ctypes.POINTER(DseErr)]),
     ("dse_debug_pairwise_sum", ctypes.c_int, [ctypes.c_int, f64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                               ctypes.c_int64, f64p, f64p, ctypes.POINTER(DseErr)]),
+    ("dse_sharded_set_stop", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    ("dse_sharded_assemble_step", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                                 ctypes.c_double, ctypes.c_double, ctypes.c_int64, ctypes.c_void_p,
+                                                 ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                 ctypes.POINTER(DseErr)]),
     ("dse_debug_exp_neg_k2", ctypes.c_int, [ctypes.c_int, ctypes.c_double, f64p, ctypes.c_int64, f64p, f64p,
                                             ctypes.POINTER(DseErr)]),
     ("dse_plan_info", ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, i32p, i32p, ctypes.c_int64, i32p, i32p, i32p,

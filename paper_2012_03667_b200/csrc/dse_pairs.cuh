@@ -60,6 +60,7 @@ constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
 // that accumulating r-weighted moments avoids.  Not built.)
 
 __global__ void __launch_bounds__(kPairsThreads, DSE_PAIRS_MINB) dse_pairs_kernel(SweepArgs a) {
+    if (a.stop && *a.stop) return;  // sharded solve already stopped (uniform over the grid)
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm[];
     double* q2 = sm;

@@ -111,6 +111,49 @@ class ShardedLoop:
         return [float(x) for x in pa] + [float(x) for x in pb]
 
 
+@dataclass
+class WindowedStopLoop:
+    """successive_approximation (iteration.py:18-40) driven from the host in
+    windows, with the stop test on the device -- the loop of the public
+    multi-GPU solve (ShardedSolver).
+
+    step(n): enqueue iteration n (sweep of the owned rows, exchange,
+        assemble + relaxation, history row n, device stop flag: 1 = both
+        deltas < xi, 2 = non-finite sweep; once set, later steps are no-ops
+        on the device, so the state stays the stopping iteration's).
+    read(lo, hi) -> (rows [hi-lo+1, W], flag): history rows lo..hi and the
+        flag, one device->host copy (the only sync of a window).
+    locate() -> (row, radial, angular): collective; the lowest failing row
+        over all ranks (every rank gets the same answer).
+
+    No collective is needed for the stop decision: every rank holds the
+    same full iterate, so the deltas and the flag agree bitwise."""
+
+    step: Callable
+    read: Callable
+    locate: Callable
+
+    def run(self, xi: float, cap: int, window: int = 16):
+        from .errors import NumericalFailureError
+        done = 0
+        while done < cap:
+            w = min(window, cap - done)
+            for n in range(done + 1, done + w + 1):
+                self.step(n)
+            rows, flag = self.read(done + 1, done + w)
+            if flag == 2:
+                bad = next(int(r[0]) for r in rows if not (np.isfinite(r[1]) and np.isfinite(r[2])))
+                row, radial, angular = self.locate()
+                raise NumericalFailureError(f"non-finite integrand in sweep at row={row}, radial={radial}, "
+                                            f"angular={angular}", row=row, radial=radial, angular=angular,
+                                            iteration=bad)
+            for r in rows:
+                if r[1] < xi and r[2] < xi:  # strict, both (iteration.py:38)
+                    return int(r[0]), True
+            done += w
+        return cap, False
+
+
 def _torch_env():
     import torch
     import torch.distributed as dist
@@ -119,91 +162,22 @@ def _torch_env():
     return torch, dist
 
 
-_LOOP_CACHE: dict = {}
-
-
-def _device_loop(grid, params, variant):
-    """ShardedLoop wiring (sweeper, rows, buffers, gather, probes), cached per
-    (grid, params, variant, rank, world) like the single-GPU sweeper cache
-    (solver._make_sweeper): repeated iterate_once / solve calls under
-    torchrun reuse the uploaded grid and plan."""
-    from .solver import _params_key
-    torch, dist = _torch_env()
-    key = (id(grid), _params_key(params), variant.interp, variant.arith, dist.get_rank(), dist.get_world_size(),
-           int(os.environ.get("LOCAL_RANK", torch.cuda.current_device())))
-    hit = _LOOP_CACHE.get(key)
-    if hit is not None and hit[0].grid is grid:
-        return hit
-    ctx = _device_loop_new(grid, params, variant)
-    for old in list(_LOOP_CACHE.values()):
-        old[0].close()
-    _LOOP_CACHE.clear()
-    _LOOP_CACHE[key] = ctx
-    return ctx
-
-
-def _device_loop_new(grid, params, variant):
-    """ShardedLoop wired to libdse_b200 (sweep) + NCCL all-gather + device probes."""
-    import ctypes
-
-    from . import _native as nat
-    from .solver import GpuSweeper
-    torch, dist = _torch_env()
-    rank, world = dist.get_rank(), dist.get_world_size()
-    from .solver import resolve_gpus
-    if resolve_gpus(variant) != world:
-        raise ParameterError(f"variant asks for {resolve_gpus(variant)} GPUs, world size is {world}")
-    local = int(os.environ.get("LOCAL_RANK", torch.cuda.current_device()))
-    dev = torch.device("cuda", local)
-    sw = GpuSweeper(grid, params, variant.interp, variant.arith, local, rows=(rank, world))
-    rows = torch.from_numpy(owned_rows(grid.n_ext, rank, world)).to(dev)
-    out_a = torch.empty(grid.n_ext, dtype=torch.float64, device=dev)
-    out_b = torch.empty_like(out_a)
-    p2 = torch.from_numpy(np.ascontiguousarray(grid.p2_ext)).to(dev)
-
-    def sweep_rows(a, b):
-        sw.sweep_device(a.data_ptr(), b.data_ptr(), out_a.data_ptr(), out_b.data_ptr(),
-                        torch.cuda.current_stream(dev).cuda_stream)
-        return out_a[rows], out_b[rows]
-
-    def gather(buf):
-        out = torch.empty((world, *buf.shape), dtype=buf.dtype, device=buf.device)
-        dist.all_gather_into_tensor(out, buf.contiguous())
-        return out
-
-    def probe_fn(probes_p2):
-        pr = torch.tensor(list(probes_p2), dtype=torch.float64, device=dev)
-
-        def probe(a, b):
-            if len(probes_p2) == 0:
-                return [], []
-            res = []
-            for v in (a, b):
-                o = torch.empty(len(probes_p2), dtype=torch.float64, device=dev)
-                err = nat.DseErr()
-                rc = nat.load().dse_interp_linear_batch_device(
-                    p2.data_ptr(), v.data_ptr(), grid.n_ext, pr.data_ptr(), len(probes_p2), nat.BATCH_SEARCH,
-                    o.data_ptr(), None, torch.cuda.current_stream(dev).cuda_stream, ctypes.byref(err))
-                nat.raise_for(rc, err)
-                res.append(o)  # stays on the device; read at the stop-test window
-            return res[0], res[1]
-        return probe
-
-    return sw, dev, rank, world, sweep_rows, gather, probe_fn, torch
-
-
 class FusedShardedStep:
     """One multi-GPU iteration as three device steps around the NCCL
-    all-gather (dse_sharded_sweep_pack / dse_sharded_assemble): the sweeper's
-    resident state is the full iterate, the owned rows are packed straight
-    into the send buffer, and one kernel reassembles the gathered rows with
-    the relaxation blend and the max-norm deltas.  Same arithmetic as
-    ShardedLoop.sweep + the blend + the deltas (bitwise at any world size:
-    a row is reduced by one CTA/warp set, and the blend and deltas are the
-    same per-element operations), in 4 launches + 1 collective per step."""
+    all-gather (dse_sharded_sweep_pack / dse_sharded_assemble[_step]): the
+    sweeper's resident state is the full iterate, the owned rows are packed
+    straight into the send buffer, and one kernel reassembles the gathered
+    rows with the relaxation blend and the max-norm deltas (and, inside a
+    solve, the history row and the device stop flag).  Bitwise the
+    single-GPU sweep + blend + deltas at any world size (a row is reduced by
+    one CTA/warp set; the blend and deltas are per-element operations)."""
 
     def __init__(self, sw, n: int, world: int, dev, gather_into, relaxation: float = 1.0):
+        import ctypes
+
         import torch
+
+        from . import _native as nat
         self.sw, self.n, self.world = sw, n, world
         self.per = math.ceil(n / world)
         self.send = torch.zeros((2, self.per), dtype=torch.float64, device=dev)
@@ -211,27 +185,40 @@ class FusedShardedStep:
         self.delta = torch.zeros(2, dtype=torch.float64, device=dev)
         self.gather_into = gather_into
         self.relax = relaxation
-        import ctypes
-        from . import _native as nat
-        self._nat = nat
+        self._nat, self._lib = nat, nat.load()
         pa, pb = ctypes.c_void_p(), ctypes.c_void_p()
-        nat.raise_for(nat.load().dse_sweeper_state(sw.handle, ctypes.byref(pa), ctypes.byref(pb)), nat.DseErr())
+        nat.raise_for(self._lib.dse_sweeper_state(sw.handle, ctypes.byref(pa), ctypes.byref(pb)), nat.DseErr())
         self.state_ptrs = (pa.value, pb.value)
+        self.kind = "nccl"
 
     def load(self, a, b, stream: int) -> None:
         self.sw.load_device(a.data_ptr(), b.data_ptr(), stream)
 
-    def step(self, stream: int):
+    def _assemble(self, recv_ptr: int, stream: int, relax, solve) -> None:
         import ctypes
         err = self._nat.DseErr()
-        lib = self._nat.load()
-        self._nat.raise_for(lib.dse_sharded_sweep_pack(self.sw.handle, self.send.data_ptr(), self.per, stream,
-                                                       ctypes.byref(err)), err)
+        relax = self.relax if relax is None else relax
+        if solve is None:
+            rc = self._lib.dse_sharded_assemble(self.sw.handle, recv_ptr, self.world, self.per, relax,
+                                                self.delta.data_ptr(), stream, ctypes.byref(err))
+        else:  # (xi, iteration, probes tensor, history row address)
+            xi, it, probes, row = solve
+            rc = self._lib.dse_sharded_assemble_step(self.sw.handle, recv_ptr, self.world, self.per, relax, xi, it,
+                                                     probes.data_ptr() if probes.numel() else None, probes.numel(),
+                                                     row, self.delta.data_ptr(), stream, ctypes.byref(err))
+        self._nat.raise_for(rc, err)
+
+    def step(self, stream: int, relax=None, solve=None):
+        import ctypes
+        err = self._nat.DseErr()
+        self._nat.raise_for(self._lib.dse_sharded_sweep_pack(self.sw.handle, self.send.data_ptr(), self.per, stream,
+                                                             ctypes.byref(err)), err)
         self.gather_into(self.recv, self.send)
-        self._nat.raise_for(lib.dse_sharded_assemble(self.sw.handle, self.recv.data_ptr(), self.world, self.per,
-                                                     self.relax, self.delta.data_ptr(), stream, ctypes.byref(err)),
-                            err)
+        self._assemble(self.recv.data_ptr(), stream, relax, solve)
         return self.delta
+
+    def close(self) -> None:
+        pass
 
 
 def device_view(ptr: int, n: int, device):
@@ -245,7 +232,7 @@ def device_view(ptr: int, n: int, device):
     return torch.as_tensor(_Raw(), device=device)
 
 
-class P2PShardedStep:
+class P2PShardedStep(FusedShardedStep):
     """The multi-GPU iteration with the all-gather FUSED into the sweep over
     NVLink peer memory (no NCCL on the data path): every rank maps every
     other rank's receive buffer and barrier flag (CUDA IPC handles exchanged
@@ -253,73 +240,73 @@ class P2PShardedStep:
     stores each finished row into all receive buffers the moment the row is
     done (dse_sharded_sweep_push), a one-thread kernel barriers across the
     GPUs over the flags (bounded spin: a missing peer raises instead of
-    hanging), and dse_sharded_assemble rebuilds the full iterate with the
-    blend and the deltas.  3 launches per step."""
+    hanging), and the assemble kernel rebuilds the full iterate.  3 launches
+    per step.
+
+    Construction is collective and failure-safe: every rank makes exactly
+    two `exchange` calls whatever fails locally (the IPC handles, then the
+    verdict of mapping every peer), so a failure anywhere raises
+    ExecutionEnvironmentError on EVERY rank and every rank frees what it
+    allocated or mapped."""
 
     def __init__(self, sw, n: int, world: int, rank: int, device: int, dev, exchange, relaxation: float = 1.0):
         import ctypes
 
         import torch
-
-        from . import _native as nat
         if world > 8:
             raise ParameterError("the peer-memory all-gather maps at most 8 GPUs (one node)")
-        self._nat, self._lib = nat, nat.load()
-        self.sw, self.n, self.world, self.rank, self.relax = sw, n, world, rank, relaxation
-        self.per = math.ceil(n / world)
-        err = nat.DseErr()
-        self._own = []
-        handles = []
+        super().__init__(sw, n, world, dev, None, relaxation)
+        nat, lib = self._nat, self._lib
+        self.rank = rank
+        self.kind = "p2p"
         # receive buffers double-buffered by step parity: a fast rank's push of
         # step e+1 must not overwrite what a slow rank still assembles of step e
-        # (the push of e+2 waits for everyone's push of e+1, which follows
-        # their assemble of e in stream order)
         self._slot = world * 2 * self.per
-        # collective-safe construction: every rank makes exactly one
-        # `exchange` call whatever fails locally, and an allocation or
-        # mapping failure is reported through it (no rank is left waiting)
-        local_error = None
+        self._own, self._mapped = [], []
+        err = nat.DseErr()
+        local_error, handles = None, []
         try:
             for nbytes in (2 * self._slot * 8, 64):
                 ptr = ctypes.c_void_p()
                 h = ctypes.create_string_buffer(64)
-                nat.raise_for(self._lib.dse_p2p_alloc(device, nbytes, ctypes.byref(ptr), h, ctypes.byref(err)), err)
+                nat.raise_for(lib.dse_p2p_alloc(device, nbytes, ctypes.byref(ptr), h, ctypes.byref(err)), err)
                 self._own.append(ptr.value)
                 handles.append(h.raw)
-        except Exception as exc:  # noqa: BLE001
+        except Exception as exc:  # noqa: BLE001 -- reported through the exchange
             local_error = f"{type(exc).__name__}: {exc}"
         everyone = exchange((local_error, tuple(handles)))
         bad = [f"rank {q}: {e}" for q, (e, _) in enumerate(everyone) if e is not None]
-        self._mapped = []
+        recv, flags = [], []
+        if not bad:
+            try:
+                for q in range(world):
+                    if q == rank:
+                        recv.append(self._own[0])
+                        flags.append(self._own[1])
+                        continue
+                    got = []
+                    for k in range(2):
+                        ptr = ctypes.c_void_p()
+                        nat.raise_for(lib.dse_p2p_open(device, everyone[q][1][k], ctypes.byref(ptr),
+                                                       ctypes.byref(err)), err)
+                        got.append(ptr.value)
+                        self._mapped.append(ptr.value)
+                    recv.append(got[0])
+                    flags.append(got[1])
+            except Exception as exc:  # noqa: BLE001
+                local_error = f"{type(exc).__name__}: {exc}"
+            verdict = exchange(local_error)  # second collective: the mapping verdict of every rank
+            bad = [f"rank {q}: {e}" for q, e in enumerate(verdict) if e is not None]
         if bad:
             self.close()
             raise ExecutionEnvironmentError("peer-memory setup failed on " + "; ".join(bad))
-        recv, flags = [], []
-        for q in range(world):
-            if q == rank:
-                recv.append(self._own[0])
-                flags.append(self._own[1])
-                continue
-            got = []
-            for k in range(2):
-                ptr = ctypes.c_void_p()
-                nat.raise_for(self._lib.dse_p2p_open(device, everyone[q][1][k], ctypes.byref(ptr),
-                                                     ctypes.byref(err)), err)
-                got.append(ptr.value)
-                self._mapped.append(ptr.value)
-            recv.append(got[0])
-            flags.append(got[1])
         self.peer_recv = [(ctypes.c_uint64 * world)(*[r + 8 * self._slot * par for r in recv]) for par in (0, 1)]
         self.peer_flags = (ctypes.c_uint64 * world)(*flags)
         self.recv_local = [self._own[0] + 8 * self._slot * par for par in (0, 1)]
         self.epoch = 0
         self.timed_out = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.delta = torch.zeros(2, dtype=torch.float64, device=dev)
 
-    def load(self, a, b, stream: int) -> None:
-        self.sw.load_device(a.data_ptr(), b.data_ptr(), stream)
-
-    def step(self, stream: int):
+    def step(self, stream: int, relax=None, solve=None):
         import ctypes
         err = self._nat.DseErr()
         lib = self._lib
@@ -329,41 +316,215 @@ class P2PShardedStep:
         self.epoch += 1
         self._nat.raise_for(lib.dse_p2p_barrier(self.peer_flags, self.world, self.rank, self.epoch,
                                                 self.timed_out.data_ptr(), stream, ctypes.byref(err)), err)
-        self._nat.raise_for(lib.dse_sharded_assemble(self.sw.handle, self.recv_local[par], self.world, self.per,
-                                                     self.relax, self.delta.data_ptr(), stream, ctypes.byref(err)),
-                            err)
+        self._assemble(self.recv_local[par], stream, relax, solve)
         return self.delta
 
     def close(self) -> None:
-        for p in self._mapped:
-            self._lib.dse_p2p_close(p, 0)
-        for p in self._own:
-            self._lib.dse_p2p_close(p, 1)
+        for q in self._mapped:
+            self._lib.dse_p2p_close(q, 0)
+        for q in self._own:
+            self._lib.dse_p2p_close(q, 1)
         self._mapped, self._own = [], []
 
 
-def solve_sharded(grid, params, variant, a0, b0, probes_p2):
-    sw, dev, rank, world, sweep_rows, gather, probe_fn, torch = _device_loop(grid, params, variant)
+def select_stepper(sw, n: int, world: int, rank: int, local: int, dev, dist, probe_state=None):
+    """The multi-GPU step a solve (and the torchrun bench) runs: the
+    peer-memory step when the sweeper uses the pairs arithmetic, DSE_P2P is
+    not 0, every rank maps its peers, and one step from `probe_state` agrees
+    BITWISE with the NCCL step on every rank (and no barrier timed out);
+    else the NCCL step.  Every rank runs the same collectives on every path.
+    Returns (stepper, note)."""
+    import torch
+    from . import _native as nat
+
+    def gather_into(out, buf):
+        dist.all_gather_into_tensor(out, buf)
+
+    fused = FusedShardedStep(sw, n, world, dev, gather_into)
+    if os.environ.get("DSE_P2P", "1") == "0":
+        return fused, "NCCL all-gather (DSE_P2P=0)"
+    if sw.arith_code != nat.ARITH_PAIRS:
+        return fused, "NCCL all-gather (the fused peer-memory push needs the pairs arithmetic)"
+
+    def exchange(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
     try:
-        loop = ShardedLoop(grid.n_ext, rank, world, sweep_rows, gather, probe_fn(probes_p2), xp=torch)
-        a = torch.from_numpy(np.ascontiguousarray(a0, dtype=np.float64)).to(dev)
-        b = torch.from_numpy(np.ascontiguousarray(b0, dtype=np.float64)).to(dev)
-        a, b, n, conv, hist = loop.run(a, b, params.xi, int(params.max_iterations), params.relaxation)
-        return a.cpu().numpy(), b.cpu().numpy(), n, conv, hist
-    finally:
-        pass  # the sweeper stays cached (_LOOP_CACHE)
+        p2p = P2PShardedStep(sw, n, world, rank, local, dev, exchange)
+    except ExecutionEnvironmentError as exc:  # raised on every rank together
+        return fused, f"NCCL all-gather (peer memory: {str(exc)[:120]})"
+    sp = torch.cuda.current_stream(dev).cuda_stream
+    a, b = probe_state if probe_state is not None else (
+        torch.ones(n, dtype=torch.float64, device=dev), torch.full((n,), 0.3, dtype=torch.float64, device=dev))
+    ok_here, why = 0, "peer-memory step disagreed with the NCCL step or timed out on some rank"
+    try:
+        fused.load(a, b, sp)
+        fused.step(sp)
+        ref = torch.cat([device_view(fused.state_ptrs[0], n, dev), device_view(fused.state_ptrs[1], n, dev)]).clone()
+        p2p.load(a, b, sp)
+        p2p.step(sp)
+        got = torch.cat([device_view(fused.state_ptrs[0], n, dev), device_view(fused.state_ptrs[1], n, dev)])
+        torch.cuda.synchronize()
+        ok_here = int(bool(torch.equal(got, ref)) and int(p2p.timed_out.item()) == 0)
+    except Exception as exc:  # noqa: BLE001
+        ok_here, why = 0, f"{type(exc).__name__}: {str(exc)[:120]}"
+    flag = torch.tensor([ok_here], device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 1:
+        return p2p, "peer-memory all-gather fused into the sweep (validated bitwise against the NCCL step)"
+    torch.cuda.synchronize()
+    dist.barrier()  # no peer may unmap a buffer another rank still writes
+    p2p.close()
+    return fused, f"NCCL all-gather ({why})"
+
+
+class ShardedSolver:
+    """The public multi-GPU path (solve / iterate_once with gpus = W under
+    torchrun): rank r owns rows r, r+W, ... of a row-sharded sweeper; one
+    iteration is the selected step (peer-memory push or NCCL all-gather)
+    with relaxation, deltas, history row and stop flag on the device;
+    WindowedStopLoop reads the history once per window.  Iterations queued
+    past the stop inside a window are no-ops on the device (the stop flag),
+    so nothing is computed past convergence and the result (state,
+    iterations, history) is that of the eager loop and bitwise the
+    single-GPU solve's.  A non-finite sweep stops every rank at the same
+    iteration and every rank raises the same NumericalFailureError (lowest
+    failing row over the ranks)."""
+
+    def __init__(self, grid, params, variant, window: int = 16):
+        from .solver import GpuSweeper, resolve_gpus
+        torch, dist = _torch_env()
+        self.torch, self.dist = torch, dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        if resolve_gpus(variant) != self.world:
+            raise ParameterError(f"variant asks for {resolve_gpus(variant)} GPUs, world size is {self.world}")
+        self.local = int(os.environ.get("LOCAL_RANK", torch.cuda.current_device()))
+        self.dev = torch.device("cuda", self.local)
+        self.grid, self.params, self.window = grid, params, window
+        self.n = grid.n_ext
+        self.sw = GpuSweeper(grid, params, variant.interp, variant.arith, self.local, rows=(self.rank, self.world))
+        self.stepper, self.note = select_stepper(self.sw, self.n, self.world, self.rank, self.local, self.dev, dist)
+        self.stop = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self._lib = self.sw.lib
+
+    @property
+    def stream(self) -> int:
+        return self.torch.cuda.current_stream(self.dev).cuda_stream
+
+    def _state(self):
+        ptrs = self.stepper.state_ptrs
+        return (device_view(ptrs[0], self.n, self.dev).cpu().numpy(),
+                device_view(ptrs[1], self.n, self.dev).cpu().numpy())
+
+    def locate(self):
+        """Collective: (row, radial, angular) of the lowest failing row."""
+        from .errors import NumericalFailureError
+        torch = self.torch
+        mine = [np.iinfo(np.int64).max, -1, -1]
+        try:
+            self.sw.check()
+        except NumericalFailureError as exc:
+            mine = [int(exc.row), int(exc.radial), int(exc.angular)]
+        t = torch.tensor(mine, dtype=torch.int64, device=self.dev)
+        out = torch.empty((self.world, 3), dtype=torch.int64, device=self.dev)
+        self.dist.all_gather_into_tensor(out, t)
+        rows = out.cpu().numpy()
+        best = rows[np.argmin(rows[:, 0])]
+        return int(best[0]), int(best[1]), int(best[2])
+
+    def _load(self, a, b):
+        torch = self.torch
+        ta = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(self.dev)
+        tb = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).to(self.dev)
+        self.stepper.load(ta, tb, self.stream)
+
+    def solve(self, a0, b0, probes_p2, xi: float, cap: int, relaxation: float):
+        import ctypes
+        torch = self.torch
+        P = len(probes_p2)
+        W = 3 + 2 * P
+        hist = torch.full((cap + 1, W), float("nan"), dtype=torch.float64, device=self.dev)
+        probes = torch.tensor(list(probes_p2), dtype=torch.float64, device=self.dev)
+        self._load(a0, b0)
+        self.stop.zero_()
+        nat = self.sw.lib
+        nat.dse_sharded_set_stop(self.sw.handle, ctypes.c_void_p(self.stop.data_ptr()))
+        row_bytes = W * 8
+        base = hist.data_ptr()
+        try:
+            def step(n):
+                self.stepper.step(self.stream, relaxation, (xi, n, probes, base + n * row_bytes))
+
+            def read(lo, hi):
+                rows = hist[lo:hi + 1].cpu().numpy()  # stream-ordered after the window's steps
+                return rows, int(self.stop.item())
+            n, conv = WindowedStopLoop(step, read, self.locate).run(xi, cap, self.window)
+        finally:
+            nat.dse_sharded_set_stop(self.sw.handle, None)
+        a, b = self._state()
+        h = hist[: n + 1].cpu().numpy()
+        h[0, 0], h[0, 1], h[0, 2] = 0.0, np.nan, np.nan
+        if P:
+            from .interpolation import interp_search_many
+            h[0, 3:3 + P] = interp_search_many(self.grid.p2_ext, a0, list(probes_p2))
+            h[0, 3 + P:] = interp_search_many(self.grid.p2_ext, b0, list(probes_p2))
+        return a, b, n, conv, h
+
+    def sweep(self, a, b):
+        """One sweep (iterate_once): the solve loop capped at one iteration
+        with xi = 0 (never met: deltas are >= 0), so a non-finite sweep
+        leaves the input state in place for the failure location and every
+        rank raises the same NumericalFailureError (without iteration)."""
+        from .errors import NumericalFailureError
+        try:
+            a1, b1, _, _, _ = self.solve(a, b, (), 0.0, 1, 1.0)
+        except NumericalFailureError as exc:
+            exc.iteration = None
+            raise
+        return a1, b1
+
+    def close(self) -> None:
+        self.torch.cuda.synchronize()
+        if self.world > 1:
+            self.dist.barrier()  # no peer may unmap a buffer another rank still writes
+        self.stepper.close()
+        self.sw.close()
+
+
+_SOLVERS: dict = {}
+
+
+def sharded_solver(grid, params, variant) -> ShardedSolver:
+    """ShardedSolver cached per (grid, params, variant, rank, world, device)
+    like the single-GPU sweeper cache (solver._make_sweeper): repeated
+    iterate_once / solve calls under torchrun reuse the uploaded grid, the
+    plan and the peer mappings."""
+    from .solver import _params_key
+    torch, dist = _torch_env()
+    key = (id(grid), _params_key(params), variant.interp, variant.arith, dist.get_rank(), dist.get_world_size(),
+           int(os.environ.get("LOCAL_RANK", torch.cuda.current_device())))
+    hit = _SOLVERS.get(key)
+    if hit is not None and hit.grid is grid:
+        return hit
+    close_solvers()
+    ctx = ShardedSolver(grid, params, variant)
+    _SOLVERS[key] = ctx
+    return ctx
+
+
+def close_solvers() -> None:
+    while _SOLVERS:
+        _SOLVERS.popitem()[1].close()
+
+
+def solve_sharded(grid, params, variant, a0, b0, probes_p2):
+    ctx = sharded_solver(grid, params, variant)
+    return ctx.solve(a0, b0, probes_p2, float(params.xi), int(params.max_iterations), float(params.relaxation))
 
 
 def iterate_once_sharded(grid, a, b, params, variant):
-    sw, dev, rank, world, sweep_rows, gather, probe_fn, torch = _device_loop(grid, params, variant)
-    try:
-        loop = ShardedLoop(grid.n_ext, rank, world, sweep_rows, gather, probe_fn(()), xp=torch)
-        at = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
-        bt = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).to(dev)
-        an, bn = loop.sweep(at, bt)
-        return an.cpu().numpy(), bn.cpu().numpy()
-    finally:
-        pass  # the sweeper stays cached (_LOOP_CACHE)
+    return sharded_solver(grid, params, variant).sweep(a, b)
 
 
 def bench_main(args, metric, unit, cfg, flop_per_point):
@@ -387,6 +548,9 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
     sys.stdout.flush()
     saved_stdout = os.dup(1)
     os.dup2(2, 1)
+    # NCCL's communicator lines (rank count per communicator) on stderr
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     dist.init_process_group("nccl")
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -395,70 +559,30 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
     grid = build_grid(cfg["N"], cfg["M"], cfg["K"], cfg["p2_min"], cfg["p2_max"])
     params = ModelParams(N=cfg["N"], m_rad=cfg["M"], m_ang=cfg["K"], xi=1e-10)
     variant = VARIANTS["indexed-gpu-pairs"].with_gpus(world)
-    sw, dev, rank, world, sweep_rows, gather, probe_fn, torch = _device_loop(grid, params, variant)
-
-    def gather_into(out, buf):
-        dist.all_gather_into_tensor(out, buf)
-
-    fused = FusedShardedStep(sw, grid.n_ext, world, dev, gather_into)
+    # the public path's own solver object: the step timed here is the one
+    # solve() / iterate_once() run (peer-memory push when it validates)
+    ctx = sharded_solver(grid, params, variant)
+    sw, dev, stepper, p2p_note = ctx.sw, ctx.dev, ctx.stepper, ctx.note
     a = torch.ones(grid.n_ext, dtype=torch.float64, device=dev)
     b = torch.full((grid.n_ext,), 0.3, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     sp = torch.cuda.current_stream(dev).cuda_stream
-    state_ptr = fused.state_ptrs
-    # the all-gather fused into the sweep over NVLink peer memory, if every
-    # rank validates it bitwise against the NCCL step (else the NCCL step)
-    exchanger = None
-    p2p_note = "disabled (DSE_P2P=0)"
-    if os.environ.get("DSE_P2P", "1") != "0":
-        # every rank runs the same collectives on every path: the IPC exchange
-        # (inside P2PShardedStep, which reports local failures through it) and
-        # one all_reduce of the local verdict
-        def exchange(obj):
-            out = [None] * world
-            dist.all_gather_object(out, obj)
-            return out
-        ok_here, why = 0, "setup"
-        try:
-            exchanger = P2PShardedStep(sw, grid.n_ext, world, rank, local, dev, exchange)
-        except Exception as exc:  # noqa: BLE001 -- every rank raised (the exchange told them)
-            exchanger, why = None, f"{type(exc).__name__}: {str(exc)[:120]}"
-        if exchanger is not None:
-            try:
-                fused.load(a, b, sp)
-                fused.step(sp)
-                ref = torch.cat([device_view(state_ptr[0], grid.n_ext, dev),
-                                 device_view(state_ptr[1], grid.n_ext, dev)]).clone()
-                exchanger.load(a, b, sp)
-                exchanger.step(sp)
-                got = torch.cat([device_view(state_ptr[0], grid.n_ext, dev),
-                                 device_view(state_ptr[1], grid.n_ext, dev)])
-                torch.cuda.synchronize()
-                ok_here = int(bool(torch.equal(got, ref)) and int(exchanger.timed_out.item()) == 0)
-                why = "peer-memory step disagreed with the NCCL step or timed out on some rank"
-            except Exception as exc:  # noqa: BLE001
-                ok_here, why = 0, f"{type(exc).__name__}: {str(exc)[:120]}"
-            flag = torch.tensor([ok_here], device=dev)
-            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-            if int(flag.item()) == 1:
-                p2p_note = "peer-memory all-gather fused into the sweep (validated bitwise vs the NCCL step)"
-            else:
-                p2p_note = f"fallback to NCCL: {why}"
-                torch.cuda.synchronize()
-                dist.barrier()
-                exchanger.close()
-                exchanger = None
-        else:
-            p2p_note = f"fallback to NCCL: {why}"
-    stepper = exchanger if exchanger is not None else fused
+    exchanger = stepper if stepper.kind == "p2p" else None
+    # the solve's own step: assemble with relaxation, deltas, the history row
+    # (probes at the default log10 p) and the device stop flag
+    import ctypes
+    probes = torch.tensor([10.0 ** (2.0 * lp) for lp in (-2.5, 0.0)], dtype=torch.float64, device=dev)
+    hist = torch.zeros((2, 3 + 2 * probes.numel()), dtype=torch.float64, device=dev)
+    sw.lib.dse_sharded_set_stop(sw.handle, ctypes.c_void_p(ctx.stop.data_ptr()))
 
     def step():
         # every step sweeps the same synthetic state (config 2 diverges,
-        # SURVEY F3): reload (untimed below), then sweep + all-gather + assemble
-        return stepper.step(sp)
+        # SURVEY F3): reload (untimed below), then sweep + exchange + assemble
+        return stepper.step(sp, params.relaxation, (params.xi, 1, probes, hist[1].data_ptr()))
 
     for _ in range(args.warmup):
         stepper.load(a, b, sp)
+        ctx.stop.zero_()
         flush.fill_(1)
         step()
     torch.cuda.synchronize()
@@ -471,6 +595,7 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
         clk = ClockSampler(local).__enter__()
     for e0, e1 in ev:
         stepper.load(a, b, sp)
+        ctx.stop.zero_()
         flush.fill_(1)
         e0.record()
         step()
@@ -479,10 +604,13 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
     if clk is not None:
         clk.__exit__(None, None, None)
     launches = nat.launch_count() - launches0
+    sw.lib.dse_sharded_set_stop(sw.handle, None)
     dist.barrier()
-    t = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in ev) / 1e3], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t = float(t.item())
+    mine = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in ev) / 1e3], device=dev)
+    per_rank = torch.empty(world, dtype=mine.dtype, device=dev)
+    dist.all_gather_into_tensor(per_rank, mine)
+    per_rank_ms = [1e3 * float(x) / args.steps for x in per_rank.cpu()]
+    t = max(float(x) for x in per_rank.cpu())  # max over ranks
     st = sw.stats()
     evald = torch.tensor([float(st["evaluated_points"])], device=dev)
     dist.all_reduce(evald, op=dist.ReduceOp.SUM)
@@ -604,15 +732,10 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
                          "flop_per_point": flop_per_point, "points": "evaluated, per GPU",
                          "peak_source": "measured: dse_fp64_peak DFMA probe (per GPU)"},
             "gpu_launches": launches,
+            "per_rank_ms_per_step": per_rank_ms,
             "clocks": clk.summary() if clk is not None else None,
             "finite_mu": mu_block,
         }))
-    if exchanger is not None:
-        torch.cuda.synchronize()
-        dist.barrier()  # no peer may unmap a buffer another rank still writes
-        exchanger.close()
-    for ctx in list(_LOOP_CACHE.values()):
-        ctx[0].close()
-    _LOOP_CACHE.clear()
+    close_solvers()
     dist.destroy_process_group()
     return 0

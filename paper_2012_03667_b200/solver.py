@@ -273,6 +273,7 @@ class GpuSweeper:
         err = nat.DseErr()
         strat = nat.INTERP_INDEXED if strategy is InterpStrategy.PRECOMPUTED_INDEX else nat.INTERP_SEARCH
         ar = _arith_code(arith)
+        self.arith_code = ar
         rc = self.lib.dse_sweeper_create(ctypes.byref(g), ctypes.byref(prm), strat, ar, self.device,
                                          int(rows[0]), int(rows[1]), ctypes.byref(handle), ctypes.byref(err))
         nat.raise_for(rc, err)

@@ -150,3 +150,70 @@ def test_p2p_step_world1_equals_sweep(relax):
         state_a, state_b = ra, rb
     step.close()
     sw.close()
+
+
+@pytest.mark.parametrize("vname", ["indexed-gpu-pairs", "indexed-seq"])
+def test_public_sharded_solve_world1_stops_exactly(nccl_world1, vname):
+    """The public multi-GPU solve (ShardedSolver: the selected step with
+    history row and stop flag on the device, a 16-iteration host window)
+    equals the single-GPU solve bitwise -- state, iteration count, history --
+    so the iterations queued past convergence inside the window changed
+    nothing (they are device no-ops).  Relaxation 0.5 on the 256^3 grid."""
+    z = golden("solve_sub256.npz")
+    g = golden_grid("sub256")
+    prm = params_ns(xi=1e-10, relaxation=0.5, max_iterations=2000)
+    b0 = np.full(g.n_ext, 0.3)
+    ref = p.solve(prm, p.VARIANTS[vname], grid=g, b0=b0)
+    from paper_2012_03667_b200.distributed import close_solvers, solve_sharded
+    a, b, n, conv, hist = solve_sharded(g, prm, p.VARIANTS[vname].with_gpus(1), np.ones(g.n_ext), b0,
+                                        tuple(10.0 ** (2.0 * lp) for lp in (-2.5, 0.0)))
+    assert conv and n == ref.iterations == int(z["iterations"])
+    assert np.array_equal(a, ref.A) and np.array_equal(b, ref.B)
+    h_ref = np.array([[r.iteration, r.max_delta_a, r.max_delta_b, *r.probe_a, *r.probe_b] for r in ref.history])
+    assert np.array_equal(hist, h_ref, equal_nan=True)
+    close_solvers()
+
+
+def test_public_sharded_failure_matches_single_gpu(nccl_world1):
+    """A non-finite sweep inside the sharded solve raises the reference's
+    NumericalFailureError with the single-GPU solve's (iteration, row,
+    radial, angular)."""
+    g = golden_grid("small")
+    prm = params_ns(xi=1e-3, max_iterations=50)
+    a0 = np.ones(g.n_ext)
+    a0[5] = np.inf
+    with pytest.raises(p.NumericalFailureError) as ref:
+        p.solve(prm, p.VARIANTS["indexed-gpu-pairs"], grid=g, a0=a0)
+    from paper_2012_03667_b200.distributed import close_solvers, iterate_once_sharded, solve_sharded
+    with pytest.raises(p.NumericalFailureError) as got:
+        solve_sharded(g, prm, p.VARIANTS["indexed-gpu-pairs"].with_gpus(1), a0, np.ones(g.n_ext), ())
+    assert (got.value.iteration, got.value.row, got.value.radial, got.value.angular) == \
+        (ref.value.iteration, ref.value.row, ref.value.radial, ref.value.angular)
+    with pytest.raises(p.NumericalFailureError) as ref1:
+        p.iterate_once(g, a0, np.ones(g.n_ext), prm, p.VARIANTS["indexed-gpu-pairs"])
+    with pytest.raises(p.NumericalFailureError) as got1:
+        iterate_once_sharded(g, a0, np.ones(g.n_ext), prm, p.VARIANTS["indexed-gpu-pairs"].with_gpus(1))
+    assert (got1.value.row, got1.value.radial, got1.value.angular) == \
+        (ref1.value.row, ref1.value.radial, ref1.value.angular)
+    close_solvers()
+
+
+def test_torchrun_world2_public_solve_bitwise(tmp_path):
+    """W = 2 under torchrun (needs two GPUs: skipped on a one-GPU box): the
+    public solve / iterate_once with gpus=2 equal the single-GPU results
+    bitwise, through the peer-memory step and through the NCCL step."""
+    import subprocess
+    import sys
+
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for p2p in ("1", "0"):
+        env = dict(os.environ, DSE_P2P=p2p, PYTHONPATH=root)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+               os.path.join(root, "scripts", "dist_solve_check.py")]
+        res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-3000:]
+        assert "dist_solve_check ok" in res.stdout
