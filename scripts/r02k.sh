@@ -1,0 +1,6 @@
+set -u
+O=gpurun_out
+timeout 900 python -m pytest tests/test_gpu_interp.py tests/test_cubic.py -q -m gpu > $O/r02k_pytest.log 2>&1; echo "pytest rc=$?" >> $O/r02k_pytest.log
+python scripts/interp_sweep.py > $O/r02k_interp.jsonl 2>&1
+DSE_INTERP_REP=2 python scripts/interp_sweep.py >> $O/r02k_interp.jsonl 2>&1
+echo done

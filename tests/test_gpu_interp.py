@@ -60,3 +60,36 @@ def test_interp_validation():
     with pytest.raises(p.ParameterError):
         p.interp_search_many(np.array([1.0, 1.0]), np.array([1.0, 2.0]), np.array([1.0]))
     assert p.interp_search_many(np.array([1.0, 2.0]), np.array([1.0, 2.0]), np.array([])).size == 0
+
+
+@pytest.mark.parametrize("table", ["logspace", "nonuniform", "flat_pieces"])
+@pytest.mark.parametrize("mode", ["search", "direct"])
+def test_streaming_kernel_edge_cases_bitwise(table, mode, monkeypatch):
+    """The TMA-streamed kernel (tables replicated per bank group, precomputed
+    reciprocals, one-branch fast path) against the C oracle and against the
+    plain kernel (DSE_INTERP_NOSTREAM): knots, their neighbours, clamps,
+    NaN/inf, constant pieces (zero dv: the reciprocal path falls back to
+    IEEE division) -- 40k queries, so full tiles, a tail and the slow path
+    all run."""
+    rng = np.random.default_rng(31)
+    if table == "logspace":
+        x = np.logspace(-4, 4, 512)
+        v = 1.0 / (1.0 + x) + 0.1 * np.log1p(x)
+    elif table == "nonuniform":
+        x = np.cumsum(rng.exponential(1.0, 300)) + 1e-3
+        v = rng.normal(size=300)
+    else:
+        x = np.logspace(-2, 2, 64)
+        v = np.repeat(rng.normal(size=16), 4)  # constant on 3 of every 4 intervals
+    edge = np.concatenate([x, np.nextafter(x, 0), np.nextafter(x, np.inf), [0.0, -1.0, np.inf, -np.inf, np.nan],
+                           [x[0] * 0.5, x[-1] * 2.0]])
+    q = np.concatenate([np.exp(rng.uniform(np.log(x[0]) - 0.1, np.log(x[-1]) + 0.1, 40000 - edge.size)), edge])
+    rng.shuffle(q)
+    ref = oracle.interp_search_many(x, v, q)
+    ref_idx = np.clip(np.searchsorted(x, q, "right") - 1, -1, x.size - 1)
+    ref_idx[np.isnan(q)] = 0
+    got, idx = p.interp_linear_batch(x, v, q, mode=mode, with_index=True)
+    monkeypatch.setenv("DSE_INTERP_NOSTREAM", "1")
+    plain, pidx = p.interp_linear_batch(x, v, q, mode=mode, with_index=True)
+    assert np.array_equal(got, ref, equal_nan=True) and np.array_equal(plain, ref, equal_nan=True)
+    assert np.array_equal(idx, ref_idx) and np.array_equal(pidx, ref_idx)

@@ -91,3 +91,32 @@ def test_pairs_grid_size_bitwise_equal(n, m, k):
     fast = _sweep(g, prm, {}, p.Arithmetic.FAST)
     assert np.max(np.abs(ref[0] - fast[0]) / np.abs(fast[0])) < 1e-12
     assert np.max(np.abs(ref[1] - fast[1])) / np.max(np.abs(fast[1])) < 1e-12
+
+
+@pytest.mark.parametrize("arith", [p.Arithmetic.EXACT, p.Arithmetic.FAST])
+def test_cluster_layout_bitwise(arith, monkeypatch):
+    """The few-rows layouts (2-CTA clusters for the exact arithmetic, one
+    512-thread CTA per row otherwise; DSE_NO_CLUSTER forces the latter) give
+    bit-identical sweeps and solves."""
+    g = p.build_grid(128, 128, 64, 1e-6, 1e4)
+    prm = p.ModelParams(N=128, m_rad=128, m_ang=64, xi=1e-10, max_iterations=300)
+    rng = np.random.default_rng(12)
+    a, b = rng.uniform(1, 2, 128), rng.uniform(0, 1, 128)
+    outs = []
+    for env in (None, "1"):
+        if env is None:
+            monkeypatch.delenv("DSE_NO_CLUSTER", raising=False)
+        else:
+            monkeypatch.setenv("DSE_NO_CLUSTER", env)
+        sw = p.GpuSweeper(g, prm, p.InterpStrategy.PRECOMPUTED_INDEX, arith)
+        lay = sw.layout()
+        x = sw.sweep(a, b)
+        y = sw.solve(np.ones(128), np.full(128, 0.3), (1e-5, 1.0))
+        outs.append((lay, x, y))
+        sw.close()
+    if arith is p.Arithmetic.EXACT:
+        assert outs[0][0]["cluster2"] == 1 and outs[1][0]["cluster2"] == 0
+    (_, x0, y0), (_, x1, y1) = outs
+    assert np.array_equal(x0[0], x1[0]) and np.array_equal(x0[1], x1[1])
+    assert y0[2] == y1[2] and np.array_equal(y0[0], y1[0]) and np.array_equal(y0[1], y1[1])
+    assert np.array_equal(y0[4], y1[4], equal_nan=True)
