@@ -132,6 +132,8 @@ _PROTOS = [
                                                  ctypes.POINTER(DseErr)]),
     ("dse_debug_exp_neg_k2", ctypes.c_int, [ctypes.c_int, ctypes.c_double, f64p, ctypes.c_int64, f64p, f64p,
                                             ctypes.POINTER(DseErr)]),
+    ("dse_debug_exp_exact", ctypes.c_int, [ctypes.c_int, f64p, ctypes.c_int64, f64p, f64p, i32p,
+                                           ctypes.POINTER(DseErr)]),
     ("dse_plan_info", ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, i32p, i32p, ctypes.c_int64, i32p, i32p, i32p,
                                      ctypes.c_int64, i64p, i64p]),
     ("dse_debug_check_flags", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32)]),
@@ -157,6 +159,9 @@ _PROTOS = [
     ("dse_mu_batch_sweep", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DseMuParams), ctypes.c_int64,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, i64p,
                                           ctypes.POINTER(DseErr)]),
+    ("dse_mu_batch_solve", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DseMuParams), ctypes.c_int64,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, i64p,
+                                          i32p, i64p, i64p, ctypes.c_size_t, ctypes.POINTER(DseErr)]),
     ("dse_mu_sweeper_stats", ctypes.c_int, [ctypes.c_void_p, i64p, i64p, i32p, i64p]),
     ("dse_mu_aa_residual", ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -266,6 +271,18 @@ def debug_exp_neg_k2(k2, omega: float, device: int = 0):
                                      e.ctypes.data_as(f64p), _ct.byref(err))
     raise_for(rc, err)
     return t, e
+
+
+def debug_exp_exact(x, device: int = 0):
+    """Test hook (dse_debug_exp_exact): (exp_rep, CUDA exp, exp_rep valid) of x."""
+    import ctypes as _ct
+    v = np.ascontiguousarray(x, dtype=np.float64)
+    r, e, k = np.empty(v.size), np.empty(v.size), np.empty(v.size, dtype=np.int32)
+    err = DseErr()
+    rc = load().dse_debug_exp_exact(device, v.ctypes.data_as(f64p), v.size, r.ctypes.data_as(f64p),
+                                    e.ctypes.data_as(f64p), k.ctypes.data_as(i32p), _ct.byref(err))
+    raise_for(rc, err)
+    return r, e, k.astype(bool)
 
 
 def plan_info(n: int, chunk_leaves: int = 1 << 30):

@@ -830,121 +830,223 @@ __global__ void __launch_bounds__(kThreads, MOM ? DSE_MU_MOM_MINB : DSE_MU_MINB)
 }
 
 
-// ---- batched sweeps (BASELINE config 4): S independent solves on one grid,
-// one launch per sweep, in moments mode.  Every pair's five moments are read
-// once and contracted S times (each solve has its own state, node table, mu
-// and coefficient); the per-solve arithmetic and reduction order are those of
+// ---- batched solves (BASELINE config 4): S independent solves on one grid in
+// moments mode.  Every pair's five moments are read once and contracted for
+// each solve still iterating (each solve has its own state, node table, mu and
+// coefficient); the per-solve arithmetic and reduction order are those of
 // mu_solve_kernel<V, true>, so each solve's sweep is bitwise its standalone
-// moments-mode sweep.
+// moments-mode sweep.  One cooperative launch runs the whole successive
+// approximation of the group (iteration.py:18-40 per solve: max-norm deltas
+// of A, B, C, strict stop, cap -> not converged): a solve that has stopped is
+// neither swept nor written again (its state stays in the half its last sweep
+// wrote), and the launch ends when every solve has stopped or one has failed.
+// Sweep-only mode (stop = 0, one iteration) is dse_mu_batch_sweep.
 // (rejected: cp.async staging of the next pair as in mu_solve_kernel<V, true>
 // -- moments only for S = 4, moments + both node tables for S = 2 -- measured
 // slower, S = 2 2.73 -> 3.15 ms, S = 4 5.02 -> 5.32 ms per sweep)
 constexpr int kMuMaxBatch = 4;
 struct MuBatch {
-    const double2* Xin;   // [S][3][n_ext]
-    double2* Xout;        // [S][3][n_ext]
+    double2* Xh[2];       // halves [S][3][n_ext]: iteration it reads Xh[it & 1], writes Xh[(it & 1) ^ 1]
     double2* NB;          // [S][m_int][4]
-    unsigned long long* err;  // [S] lowest failing row
-    int* nonfinite;       // [S]
-    double mu[kMuMaxBatch], coeff[kMuMaxBatch], z1[kMuMaxBatch], m0z1[kMuMaxBatch];
+    unsigned long long* err;  // [2][S] lowest failing row (per iteration parity)
+    int* nonfinite;       // [2][S]
+    double* bmax;         // [gridDim][S][3] per-CTA delta maxima
+    double* hist;         // [S][hist_stride][4] (n, |dA|, |dB|, |dC|) or null
+    long long hist_stride;
+    long long* status;    // [S][4]: iterations, converged, failed iteration, failing row
+    int stop;             // 1: stop test (solve), 0: sweep only
+    double mu[kMuMaxBatch], coeff[kMuMaxBatch], z1[kMuMaxBatch], m0z1[kMuMaxBatch], xi[kMuMaxBatch];
+    long long cap[kMuMaxBatch];
 };
 
+#ifndef DSE_MU_BATCH_MINB
+#define DSE_MU_BATCH_MINB DSE_MU_MINB
+#endif
+#ifndef DSE_MU_BATCH_SMACC
+#define DSE_MU_BATCH_SMACC 0  // per-thread accumulators of S = 4 in shared memory (frees 48 registers)
+#endif
+constexpr bool kBatchSmAcc = DSE_MU_BATCH_SMACC;
+template <int S>
+__host__ __device__ constexpr size_t batch_acc_doubles() { return (kBatchSmAcc && S == 4) ? (size_t)S * 6 * kThreads : 0; }
+
 template <int V, int S>
-__global__ void __launch_bounds__(kThreads, DSE_MU_MINB) mu_batch_kernel(MuArgs a, MuBatch b) {
+__global__ void __launch_bounds__(kThreads, DSE_MU_BATCH_MINB) mu_batch_kernel(MuArgs a, MuBatch b) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) double smem[];
-    double* red = smem;                                            // kWarps * 6 * S
+    constexpr bool smacc = batch_acc_doubles<S>() > 0;
+    double* sacc = smem;                                           // [S*6][kThreads] (smacc)
+    double* red = smem + batch_acc_doubles<S>();                   // kWarps * 6 * S
     int* rlo = reinterpret_cast<int*>(red + kWarps * 6 * S);       // m_s
     int* roff = rlo + a.m_s;                                       // m_s + 1
     __shared__ RowC s_rc[S];
     __shared__ unsigned s_row;
+    __shared__ double s_d[S][3];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_ext = a.n_s * a.n_4, m_int = a.m_s * a.m_4;
-    // phase I: every solve's node table (its state, its mu)
-    for (int s = 0; s < S; ++s) {
-        MuArgs as = a;
-        as.mu = b.mu[s];
-        as.coeff = b.coeff[s];
-        as.NB = b.NB + (size_t)s * 4 * m_int;
-        build_nodes(as, b.Xin + (size_t)s * 3 * n_ext, b.nonfinite + s);
-    }
-    grid.sync();
     int top = 1;
     while (top < a.m_s) top <<= 1;
-    for (;;) {
-        if (tid == 0) s_row = atomicAdd(a.ctr, 1u);
-        __syncthreads();
-        const unsigned r = s_row;
-        __syncthreads();
-        if (r >= (unsigned)a.n_rows) break;
-        const int i = a.row_start + (int)r * a.row_stride;
-        if (tid < S) {
-            MuArgs as = a;
-            as.mu = b.mu[tid];
-            as.coeff = b.coeff[tid];
-            s_rc[tid] = row_consts(as, b.Xin + (size_t)tid * 3 * n_ext, n_ext, i);
-        }
-        for (int js = tid; js < a.m_s; js += kThreads) rlo[js] = __ldg(a.mo_rlo + (size_t)r * a.m_s + js);
-        for (int js = tid; js <= a.m_s; js += kThreads) roff[js] = __ldg(a.mo_roff + (size_t)r * (a.m_s + 1) + js);
-        __syncthreads();
-        const int total = roff[a.m_s];
-        const long long mbase = __ldg(a.mo_base + r);
-        double acc[S][6];
-#pragma unroll
-        for (int s = 0; s < S; ++s)
-#pragma unroll
-            for (int c = 0; c < 6; ++c) acc[s][c] = 0.0;
-        for (int f0 = 0; f0 < total; f0 += kThreads) {
-            const int f = min(f0 + tid, total - 1);
-            const int js = node_of(roff, a.m_s, top, f);
-            const int j4 = rlo[js] + (f - roff[js]);
-            DCHECK(total == 0 || (js >= 0 && js < a.m_s && j4 >= 0 && j4 < a.m_4), 24);
-            double mom[5];
-            for (int q = 0; q < 5; ++q) mom[q] = __ldcs(a.mo_mom + q * a.mo_stride + mbase + f);
-            __syncwarp();
-#pragma unroll
+    unsigned act = (1u << S) - 1u;  // solves still iterating (uniform over the grid)
+    for (int it = a.it_begin; it < a.it_end && act; ++it) {
+        const int cur = it & 1;
+        const double2* Xin = b.Xh[cur];
+        double2* Xout = b.Xh[cur ^ 1];
+        if (blockIdx.x == 0 && tid == 0) {  // the next iteration's slots (unused until after this one's barriers)
+            a.ctr[cur ^ 1] = 0u;
             for (int s = 0; s < S; ++s) {
-                const double2* nb = b.NB + (size_t)s * 4 * m_int + 4 * (size_t)(js * a.m_4 + j4);
-                const double2 vn[4] = {nb[0], nb[1], nb[2], nb[3]};
-                double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-                pair_contract<V>(a, s_rc[s], js, j4, vn, mom, part);
-                if (f0 + tid < total)
-                    for (int c = 0; c < 6; ++c) acc[s][c] += part[c];
+                b.err[(cur ^ 1) * S + s] = ~0ull;
+                b.nonfinite[(cur ^ 1) * S + s] = 0;
             }
         }
-        // fixed-order block reduction per solve (mu_solve_kernel's)
+        // phase I: every iterating solve's node table (its state, its mu)
+        for (int s = 0; s < S; ++s) {
+            if (!(act >> s & 1u)) continue;
+            MuArgs as = a;
+            as.mu = b.mu[s];
+            as.coeff = b.coeff[s];
+            as.NB = b.NB + (size_t)s * 4 * m_int;
+            build_nodes(as, Xin + (size_t)s * 3 * n_ext, b.nonfinite + cur * S + s);
+        }
+        grid.sync();
+        double dmax[3] = {0.0, 0.0, 0.0};  // thread s < S: solve s's deltas over this CTA's rows
+        for (;;) {
+            if (tid == 0) s_row = atomicAdd(a.ctr + cur, 1u);
+            __syncthreads();
+            const unsigned r = s_row;
+            __syncthreads();
+            if (r >= (unsigned)a.n_rows) break;
+            const int i = a.row_start + (int)r * a.row_stride;
+            if (tid < S && (act >> tid & 1u)) {
+                MuArgs as = a;
+                as.mu = b.mu[tid];
+                as.coeff = b.coeff[tid];
+                s_rc[tid] = row_consts(as, Xin + (size_t)tid * 3 * n_ext, n_ext, i);
+            }
+            for (int js = tid; js < a.m_s; js += kThreads) rlo[js] = __ldg(a.mo_rlo + (size_t)r * a.m_s + js);
+            for (int js = tid; js <= a.m_s; js += kThreads) roff[js] = __ldg(a.mo_roff + (size_t)r * (a.m_s + 1) + js);
+            __syncthreads();
+            const int total = roff[a.m_s];
+            const long long mbase = __ldg(a.mo_base + r);
+            double acc[smacc ? 1 : S][6];
 #pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int c = 0; c < 6; ++c) {
+                    if (smacc) sacc[(s * 6 + c) * kThreads + tid] = 0.0;
+                    else acc[smacc ? 0 : s][c] = 0.0;
+                }
+            for (int f0 = 0; f0 < total; f0 += kThreads) {
+                const int f = min(f0 + tid, total - 1);
+                const int js = node_of(roff, a.m_s, top, f);
+                const int j4 = rlo[js] + (f - roff[js]);
+                DCHECK(total == 0 || (js >= 0 && js < a.m_s && j4 >= 0 && j4 < a.m_4), 24);
+                double mom[5];
+                for (int q = 0; q < 5; ++q) mom[q] = __ldcs(a.mo_mom + q * a.mo_stride + mbase + f);
+                __syncwarp();
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (!(act >> s & 1u)) continue;
+                    const double2* nb = b.NB + (size_t)s * 4 * m_int + 4 * (size_t)(js * a.m_4 + j4);
+                    const double2 vn[4] = {nb[0], nb[1], nb[2], nb[3]};
+                    double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                    pair_contract<V>(a, s_rc[s], js, j4, vn, mom, part);
+                    if (f0 + tid < total)
+                        for (int c = 0; c < 6; ++c) {
+                            if (smacc) sacc[(s * 6 + c) * kThreads + tid] += part[c];
+                            else acc[smacc ? 0 : s][c] += part[c];
+                        }
+                }
+            }
+            // fixed-order block reduction per solve (mu_solve_kernel's)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int c = 0; c < 6; ++c) {
+                    double v = smacc ? sacc[(s * 6 + c) * kThreads + tid] : acc[smacc ? 0 : s][c];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    if (lane == 0) red[(warp * S + s) * 6 + c] = v;
+                }
+            __syncthreads();
+            if (tid < S && (act >> tid & 1u)) {
+                const int s = tid;
+                const RowC& rc = s_rc[s];
+                double sum[6];
+                for (int c = 0; c < 6; ++c) {
+                    double v = red[s * 6 + c];
+                    for (int w = 1; w < kWarps; ++w) v += red[(w * S + s) * 6 + c];
+                    sum[c] = v;
+                }
+                const double2 An = make_double2(b.z1[s] + sum[0] / rc.P2, sum[1] / rc.P2);
+                const double2 Bn = make_double2(b.m0z1[s] + sum[2], sum[3]);
+                const cplx cn = C(sum[4], sum[5]) * rcp(rc.p4t);
+                const double2 Cn = make_double2(b.z1[s] + cn.x, cn.y);
+                const bool fin = isfinite(An.x) && isfinite(An.y) && isfinite(Bn.x) && isfinite(Bn.y) &&
+                                 isfinite(Cn.x) && isfinite(Cn.y);
+                const int nf = b.nonfinite[cur * S + s];
+                if (!fin || nf) atomicMin(b.err + cur * S + s, (unsigned long long)(nf ? a.row_start : i));
+                double2* Xo = Xout + (size_t)s * 3 * n_ext;
+                Xo[i] = An;
+                Xo[n_ext + i] = Bn;
+                Xo[2 * n_ext + i] = Cn;
+                // the single solve's stop-rule deltas (mu_solve_kernel)
+                dmax[0] = fmax(dmax[0], hyp(An.x - rc.Ap.x, An.y - rc.Ap.y));
+                dmax[1] = fmax(dmax[1], hyp(Bn.x - rc.Bp.x, Bn.y - rc.Bp.y));
+                dmax[2] = fmax(dmax[2], hyp(Cn.x - rc.Cp.x, Cn.y - rc.Cp.y));
+            }
+            __syncthreads();
+        }
+        if (!b.stop) break;
+        if (tid < S)
+            for (int c = 0; c < 3; ++c) b.bmax[((size_t)blockIdx.x * S + tid) * 3 + c] = dmax[c];
+        grid.sync();
+        // ---- stop test per solve (every CTA, identical decisions) ----
+        if (warp < S) {
+            double d[3] = {0.0, 0.0, 0.0};
+            for (int q = lane; q < (int)gridDim.x; q += 32)
+                for (int c = 0; c < 3; ++c) d[c] = fmax(d[c], __ldcg(b.bmax + ((size_t)q * S + warp) * 3 + c));
+            for (int c = 0; c < 3; ++c) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) d[c] = fmax(d[c], __shfl_xor_sync(0xffffffffu, d[c], o));
+                if (lane == 0) s_d[warp][c] = d[c];
+            }
+        }
+        __syncthreads();
+        bool failed = false;
         for (int s = 0; s < S; ++s)
-#pragma unroll
-            for (int c = 0; c < 6; ++c) {
-                double v = acc[s][c];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (lane == 0) red[(warp * S + s) * 6 + c] = v;
+            if ((act >> s & 1u) && __ldcg(b.err + cur * S + s) != ~0ull) failed = true;
+        const unsigned act_in = act;
+        for (int s = 0; s < S; ++s) {
+            if (!(act_in >> s & 1u)) continue;
+            const unsigned long long er = __ldcg(b.err + cur * S + s);
+            const double d0 = s_d[s][0], d1 = s_d[s][1], d2 = s_d[s][2];
+            if (er != ~0ull) {
+                if (blockIdx.x == 0 && tid == 0) {
+                    b.status[4 * s + 0] = it + 1;
+                    b.status[4 * s + 2] = it + 1;
+                    b.status[4 * s + 3] = (long long)er;
+                }
+                continue;
             }
-        __syncthreads();
-        if (tid < S) {
-            const int s = tid;
-            const RowC& rc = s_rc[s];
-            double sum[6];
-            for (int c = 0; c < 6; ++c) {
-                double v = red[s * 6 + c];
-                for (int w = 1; w < kWarps; ++w) v += red[(w * S + s) * 6 + c];
-                sum[c] = v;
+            if (blockIdx.x == 0 && tid == 0 && b.hist) {
+                double* h = b.hist + ((size_t)s * b.hist_stride + (it + 1)) * 4;
+                h[0] = double(it + 1);
+                h[1] = d0;
+                h[2] = d1;
+                h[3] = d2;
             }
-            const double2 An = make_double2(b.z1[s] + sum[0] / rc.P2, sum[1] / rc.P2);
-            const double2 Bn = make_double2(b.m0z1[s] + sum[2], sum[3]);
-            const cplx cn = C(sum[4], sum[5]) * rcp(rc.p4t);
-            const double2 Cn = make_double2(b.z1[s] + cn.x, cn.y);
-            const bool fin = isfinite(An.x) && isfinite(An.y) && isfinite(Bn.x) && isfinite(Bn.y) &&
-                             isfinite(Cn.x) && isfinite(Cn.y);
-            if (!fin || b.nonfinite[s]) atomicMin(b.err + s, (unsigned long long)(b.nonfinite[s] ? a.row_start : i));
-            double2* Xo = b.Xout + (size_t)s * 3 * n_ext;
-            Xo[i] = An;
-            Xo[n_ext + i] = Bn;
-            Xo[2 * n_ext + i] = Cn;
+            const bool conv = d0 < b.xi[s] && d1 < b.xi[s] && d2 < b.xi[s];
+            if (conv || it + 1 >= b.cap[s]) {
+                act &= ~(1u << s);
+                if (blockIdx.x == 0 && tid == 0) {
+                    b.status[4 * s + 0] = it + 1;
+                    b.status[4 * s + 1] = conv ? 1 : 0;
+                }
+            } else if (blockIdx.x == 0 && tid == 0) {
+                b.status[4 * s + 0] = it + 1;
+            }
         }
-        __syncthreads();
+        if (failed) break;
+        __syncthreads();  // s_d is rewritten by the next stop test only after two grid barriers
     }
 }
 
@@ -1131,6 +1233,9 @@ struct dse_mu_sweeper {
     unsigned long long* d_berr = nullptr;
     int* d_bnf = nullptr;
     int bblocks[2] = {0, 0};   // cooperative grid of the batch kernels (S = 2, 4)
+    long long* d_bstatus = nullptr;  // [S][4] batched solve status
+    double* d_bbmax = nullptr;       // [blocks][S][3] batched per-CTA deltas
+    int bbmax_blocks = 0;
     long long win_pairs = 0;
 };
 
@@ -1417,7 +1522,8 @@ int dse_mu_sweeper_destroy(dse_mu_sweeper* s) {
                     (void*)s->d_brk_s, (void*)s->d_brk_4, (void*)s->d_X, (void*)s->d_NB, (void*)s->d_bmax,
                     (void*)s->d_ctr, (void*)s->d_err, (void*)s->d_status, (void*)s->d_eval, (void*)s->d_hist, (void*)s->d_nonfinite,
                     (void*)s->d_mo_rlo, (void*)s->d_mo_roff, (void*)s->d_mo_base, (void*)s->d_mo_mom,
-                    (void*)s->d_bNB, (void*)s->d_berr, (void*)s->d_bnf})
+                    (void*)s->d_bNB, (void*)s->d_berr, (void*)s->d_bnf, (void*)s->d_bstatus,
+                    (void*)s->d_bbmax})
         if (p) cudaFree(p);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;
@@ -1634,11 +1740,23 @@ int dse_mu_sweeper_state(dse_mu_sweeper* s, double** dX) {
     return DSE_OK;
 }
 
-int dse_mu_batch_sweep(dse_mu_sweeper* s, const dse_mu_params* params, int64_t S, const double* dX_in,
-                       double* dX_out, uintptr_t stream, int64_t* failed_row, dse_err* err) {
-    ok(err);
-    if (!s || !params || !dX_in || !dX_out || !failed_row || (S != 2 && S != 4))
-        return fail(err, DSE_EPARAM, "bad argument (S must be 2 or 4)");
+}  // extern "C"
+
+namespace {
+const void* mu_batch_ptr(int vv, int64_t ss) {
+    if (ss == 2) return vv == DSE_MU_VERTEX_BC1 ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC1, 2>
+                      : vv == DSE_MU_VERTEX_BCB ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BCB, 2>
+                                                : (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC, 2>;
+    return vv == DSE_MU_VERTEX_BC1 ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC1, 4>
+         : vv == DSE_MU_VERTEX_BCB ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BCB, 4>
+                                   : (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC, 4>;
+}
+
+// Shared set-up of the batched launches: argument checks, the moment table,
+// the per-solve buffers and the cooperative grid; fills b's per-solve fields.
+int mu_batch_setup(dse_mu_sweeper* s, const dse_mu_params* params, int64_t S, mu::MuBatch& b, size_t& smem,
+                   dse_err* err) {
+    if (!s || !params || (S != 2 && S != 4)) return fail(err, DSE_EPARAM, "bad argument (S must be 2 or 4)");
     for (int64_t q = 0; q < S; ++q) {
         int rc = mu_check_params(params + q, err);
         if (rc) return rc;
@@ -1651,61 +1769,131 @@ int dse_mu_batch_sweep(dse_mu_sweeper* s, const dse_mu_params* params, int64_t S
     p0.mode = DSE_MU_MODE_MOMENTS;
     int rc = mu_build_moments(s, p0, err);
     if (rc) return rc;
-    const size_t m_int = (size_t)s->m_s * s->m_4, ne = (size_t)s->n_s * s->n_4;
-    if (!s->d_bNB) {
-        CUDA_TRY(cudaMalloc(&s->d_bNB, sizeof(double2) * 4 * m_int * mu::kMuMaxBatch));
-        CUDA_TRY(cudaMalloc(&s->d_berr, sizeof(unsigned long long) * mu::kMuMaxBatch));
-        CUDA_TRY(cudaMalloc(&s->d_bnf, sizeof(int) * mu::kMuMaxBatch));
-    }
-    const int v = (int)p0.vertex, si = S == 2 ? 0 : 1;
-    auto kp = [&](int vv, int64_t ss) -> const void* {
-        if (ss == 2) return vv == DSE_MU_VERTEX_BC1 ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC1, 2>
-                          : vv == DSE_MU_VERTEX_BCB ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BCB, 2>
-                                                    : (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC, 2>;
-        return vv == DSE_MU_VERTEX_BC1 ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC1, 4>
-             : vv == DSE_MU_VERTEX_BCB ? (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BCB, 4>
-                                       : (const void*)mu::mu_batch_kernel<DSE_MU_VERTEX_BC, 4>;
-    };
-    const size_t smem = (size_t)mu::kWarps * 6 * S * sizeof(double) + (2 * (size_t)s->m_s + 2) * sizeof(int);
+    const size_t m_int = (size_t)s->m_s * s->m_4;
+    const int si = S == 2 ? 0 : 1;
+    smem = ((S == 4 ? mu::batch_acc_doubles<4>() : mu::batch_acc_doubles<2>()) + (size_t)mu::kWarps * 6 * S) *
+               sizeof(double) + (2 * (size_t)s->m_s + 2) * sizeof(int);
     if (!s->bblocks[si]) {
         int per_sm = 1 << 30, sms = 0;
         for (int vv : {DSE_MU_VERTEX_BC, DSE_MU_VERTEX_BC1, DSE_MU_VERTEX_BCB}) {
-            CUDA_TRY(cudaFuncSetAttribute(kp(vv, S), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CUDA_TRY(cudaFuncSetAttribute(mu_batch_ptr(vv, S), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int n = 0;
-            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kp(vv, S), mu::kThreads, smem));
+            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mu_batch_ptr(vv, S), mu::kThreads, smem));
             per_sm = std::min(per_sm, n);
         }
         CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
         if (per_sm < 1) return fail(err, DSE_EENV, "batched kernel does not fit on an SM");
         s->bblocks[si] = per_sm * sms;
     }
-    cudaStream_t st = (cudaStream_t)stream;
-    mu::mu_reset_kernel<<<1, 32, 0, st>>>(s->d_ctr, s->d_err, s->d_status, s->d_nonfinite);
-    CUDA_TRY(cudaGetLastError());
-    g_launches.fetch_add(1);
-    CUDA_TRY(cudaMemsetAsync(s->d_berr, 0xff, sizeof(unsigned long long) * S, st));
-    CUDA_TRY(cudaMemsetAsync(s->d_bnf, 0, sizeof(int) * S, st));
-    mu::MuArgs a = mu_make_args(s, p0, 0, 1, false, true, false);
-    mu::MuBatch b{};
-    b.Xin = (const double2*)dX_in;
-    b.Xout = (double2*)dX_out;
+    if (!s->d_bNB) {
+        const int maxb = std::max(s->bblocks[0], s->bblocks[1]);
+        CUDA_TRY(cudaMalloc(&s->d_bNB, sizeof(double2) * 4 * m_int * mu::kMuMaxBatch));
+        CUDA_TRY(cudaMalloc(&s->d_berr, sizeof(unsigned long long) * 2 * mu::kMuMaxBatch));
+        CUDA_TRY(cudaMalloc(&s->d_bnf, sizeof(int) * 2 * mu::kMuMaxBatch));
+        CUDA_TRY(cudaMalloc(&s->d_bstatus, sizeof(long long) * 4 * mu::kMuMaxBatch));
+        (void)maxb;
+    }
+    if (s->bbmax_blocks < s->bblocks[si]) {
+        if (s->d_bbmax) cudaFree(s->d_bbmax);
+        s->d_bbmax = nullptr;
+        CUDA_TRY(cudaMalloc(&s->d_bbmax, sizeof(double) * 3 * mu::kMuMaxBatch * (size_t)s->bblocks[si]));
+        s->bbmax_blocks = s->bblocks[si];
+    }
+    b = mu::MuBatch{};
     b.NB = s->d_bNB;
     b.err = s->d_berr;
     b.nonfinite = s->d_bnf;
+    b.bmax = s->d_bbmax;
+    b.status = s->d_bstatus;
     for (int64_t q = 0; q < S; ++q) {
         b.mu[q] = params[q].mu;
         b.coeff[q] = params[q].coeff;
         b.z1[q] = params[q].z1;
         b.m0z1[q] = params[q].m0 * params[q].z1;
+        b.xi[q] = params[q].xi;
+        b.cap[q] = params[q].max_iterations;
     }
-    void* args[] = {&a, &b};
-    CUDA_TRY(cudaLaunchCooperativeKernel(kp(v, S), dim3(s->bblocks[si]), dim3(mu::kThreads), args, smem, st));
+    return DSE_OK;
+}
+
+int mu_batch_launch(dse_mu_sweeper* s, const dse_mu_params& p0, int64_t S, mu::MuBatch& b, size_t smem, int it_end,
+                    cudaStream_t st, dse_err* err) {
+    mu::mu_reset_kernel<<<1, 32, 0, st>>>(s->d_ctr, s->d_err, s->d_status, s->d_nonfinite);
+    CUDA_TRY(cudaGetLastError());
     g_launches.fetch_add(1);
+    CUDA_TRY(cudaMemsetAsync(s->d_berr, 0xff, sizeof(unsigned long long) * 2 * S, st));
+    CUDA_TRY(cudaMemsetAsync(s->d_bnf, 0, sizeof(int) * 2 * S, st));
+    CUDA_TRY(cudaMemsetAsync(s->d_bstatus, 0, sizeof(long long) * 4 * S, st));
+    dse_mu_params pm = p0;
+    pm.mode = DSE_MU_MODE_MOMENTS;
+    mu::MuArgs a = mu_make_args(s, pm, 0, it_end, false, true, false);
+    void* args[] = {&a, &b};
+    CUDA_TRY(cudaLaunchCooperativeKernel(mu_batch_ptr((int)p0.vertex, S), dim3(s->bblocks[S == 2 ? 0 : 1]),
+                                         dim3(mu::kThreads), args, smem, st));
+    g_launches.fetch_add(1);
+    return DSE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+
+int dse_mu_batch_sweep(dse_mu_sweeper* s, const dse_mu_params* params, int64_t S, const double* dX_in,
+                       double* dX_out, uintptr_t stream, int64_t* failed_row, dse_err* err) {
+    ok(err);
+    if (!dX_in || !dX_out || !failed_row) return fail(err, DSE_EPARAM, "null argument");
+    mu::MuBatch b;
+    size_t smem = 0;
+    int rc = mu_batch_setup(s, params, S, b, smem, err);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    b.Xh[0] = (double2*)dX_in;
+    b.Xh[1] = (double2*)dX_out;
+    b.stop = 0;
+    rc = mu_batch_launch(s, params[0], S, b, smem, 1, st, err);
+    if (rc) return rc;
     unsigned long long er[mu::kMuMaxBatch];
     CUDA_TRY(cudaMemcpyAsync(er, s->d_berr, sizeof(unsigned long long) * S, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    (void)ne;
     for (int64_t q = 0; q < S; ++q) failed_row[q] = er[q] == ~0ull ? -1 : (int64_t)er[q];
+    return DSE_OK;
+}
+
+int dse_mu_batch_solve(dse_mu_sweeper* s, const dse_mu_params* params, int64_t S, double* dX0, double* dX1,
+                       double* hist, int64_t hist_stride, int64_t* iterations, int32_t* converged,
+                       int64_t* failed_iteration, int64_t* failed_row, uintptr_t stream, dse_err* err) {
+    ok(err);
+    if (!dX0 || !dX1 || !iterations || !converged || !failed_iteration || !failed_row)
+        return fail(err, DSE_EPARAM, "null argument");
+    mu::MuBatch b;
+    size_t smem = 0;
+    int rc = mu_batch_setup(s, params, S, b, smem, err);
+    if (rc) return rc;
+    long long cap = 0;
+    for (int64_t q = 0; q < S; ++q) {
+        if (params[q].relaxation != 1.0)
+            return fail(err, DSE_EPARAM, "batched solves run plain successive approximation (relaxation 1)");
+        cap = std::max<long long>(cap, params[q].max_iterations);
+    }
+    if (hist && hist_stride < cap + 1) return fail(err, DSE_EPARAM, "hist_stride must be >= max_iterations + 1");
+    if (cap > (1ll << 30)) return fail(err, DSE_EPARAM, "max_iterations too large");
+    cudaStream_t st = (cudaStream_t)stream;
+    b.Xh[0] = (double2*)dX0;
+    b.Xh[1] = (double2*)dX1;
+    b.stop = 1;
+    b.hist = hist;
+    b.hist_stride = hist_stride;
+    rc = mu_batch_launch(s, params[0], S, b, smem, (int)cap, st, err);
+    if (rc) return rc;
+    long long stt[4 * mu::kMuMaxBatch];
+    CUDA_TRY(cudaMemcpyAsync(stt, s->d_bstatus, sizeof(long long) * 4 * S, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int64_t q = 0; q < S; ++q) {
+        iterations[q] = stt[4 * q + 0];
+        converged[q] = (int32_t)stt[4 * q + 1];
+        failed_iteration[q] = stt[4 * q + 2];
+        failed_row[q] = stt[4 * q + 2] ? stt[4 * q + 3] : -1;
+    }
     return DSE_OK;
 }
 

@@ -508,14 +508,13 @@ def solve_mu_batch_sa(mus, params: MuParams | None = None, grid: MuGrid | None =
     """BASELINE config 4 on one GPU by plain successive approximation -- the
     parity-equivalent path: every solve is solve_mu's loop (same sweep, same
     max-norm deltas, same strict stop rule, iteration.py:18-40), so its
-    iterations, state and history are bitwise those of the standalone solve;
-    the mu values are swept `batch` (2 or 4) at a time by dse_mu_batch_sweep,
-    which reads each pair's five moments once per group sweep (moments mode:
-    one table for all mu values, built once).  The deltas max|g(x) - x| per
-    function come from the same device kernel as the Anderson path's residual
-    (hypot of the difference, as the single-solve kernel).  A solve that has
-    converged is still swept with its group (its converged state is kept);
-    relaxation != 1 runs the solves one by one (solve_mu_batch)."""
+    iterations, state and history are bitwise those of the standalone solve.
+    The mu values run `batch` (2 or 4) at a time, each group as ONE
+    cooperative launch (dse_mu_batch_solve: the device-resident loop of the
+    single solve, run per solve) that reads each pair's five moments once per
+    group sweep (moments mode: one table for all mu values, built once) and
+    stops sweeping a solve once it has stopped; no host round trip per
+    iteration.  relaxation != 1 runs the solves one by one (solve_mu_batch)."""
     import torch
     params = MuParams() if params is None else params
     params = replace(params, mode="moments")
@@ -531,9 +530,11 @@ def solve_mu_batch_sa(mus, params: MuParams | None = None, grid: MuGrid | None =
     init = torch.cat([torch.full((n,), v, dtype=torch.complex128) for v in (1.0, 0.3, 1.0)]).to(dev)
     lib = nat.load()
     out_all = []
+    cap = params.max_iterations
     with MuSweeper(grid, params, device) as sw:
         mus = list(mus)
         st = torch.cuda.current_stream(dev).cuda_stream
+        hist = torch.full((batch, cap + 1, 4), float("nan"), dtype=torch.float64, device=dev)
         for g0 in range(0, len(mus), batch):
             group = mus[g0:g0 + batch]
             S = 4 if len(group) > 2 else 2
@@ -541,44 +542,29 @@ def solve_mu_batch_sa(mus, params: MuParams | None = None, grid: MuGrid | None =
             plist += [plist[-1]] * (S - len(plist))  # pad with a repeat (its result is dropped)
             for p_ in plist:
                 _check_c_projection(grid, p_)
-            x = init.repeat(S, 1).contiguous()
-            gx = torch.empty_like(x)
-            f = torch.empty_like(x)
-            scratch = torch.zeros(3 * S, dtype=torch.float64, device=dev)
-            host = np.zeros(3 * S)
-            nocols = np.zeros(1, dtype=np.int32)
-            hist = [[MuIterationRecord(0, float("nan"), float("nan"), float("nan"))] for _ in range(S)]
-            res = [None] * S
-            its = [params.max_iterations] * S
-            for it in range(1, params.max_iterations + 1):
-                failed = sw.batch_sweep(x, gx, plist, st)
-                for s_ in range(S):
-                    if res[s_] is None and failed[s_] >= 0:
-                        from .errors import NumericalFailureError
-                        raise NumericalFailureError(f"non-finite integrand in batched finite-mu sweep, mu="
-                                                    f"{plist[s_].mu}, row={failed[s_]}", row=failed[s_], iteration=it)
-                err = nat.DseErr()
-                # deltas only: no Anderson history (slot -1, no Gram columns)
-                nat.raise_for(lib.dse_mu_aa_residual(
-                    S, n, x.data_ptr(), gx.data_ptr(), f.data_ptr(), f.data_ptr(), f.data_ptr(), f.data_ptr(),
-                    f.data_ptr(), 1, -1, nocols.ctypes.data_as(nat.i32p), 0, scratch.data_ptr(),
-                    host.ctypes.data_as(nat.f64p), st, ctypes.byref(err)), err)
-                d = host.reshape(S, 3)
-                for s_ in range(S):
-                    if res[s_] is not None:
-                        continue
-                    hist[s_].append(MuIterationRecord(it, float(d[s_, 0]), float(d[s_, 1]), float(d[s_, 2])))
-                    if d[s_, 0] < params.xi and d[s_, 1] < params.xi and d[s_, 2] < params.xi:
-                        res[s_] = gx[s_].clone()
-                        its[s_] = it
-                x, gx = gx, x
-                if all(r is not None for r in res[:len(group)]):
-                    break
+            x0 = init.repeat(S, 1).contiguous()
+            x1 = torch.empty_like(x0)
+            cps = (nat.DseMuParams * S)(*[_c_params(p_) for p_ in plist])
+            its = (ctypes.c_int64 * S)()
+            conv = (ctypes.c_int32 * S)()
+            fit = (ctypes.c_int64 * S)()
+            frow = (ctypes.c_int64 * S)()
+            err = nat.DseErr()
+            nat.raise_for(lib.dse_mu_batch_solve(sw.handle, cps, S, x0.data_ptr(), x1.data_ptr(), hist.data_ptr(),
+                                                 cap + 1, its, conv, fit, frow, st, ctypes.byref(err)), err)
             for s_ in range(len(group)):
-                xs = (res[s_] if res[s_] is not None else x[s_]).cpu().numpy()
+                if fit[s_] > 0:
+                    raise NumericalFailureError(f"non-finite integrand in batched finite-mu sweep, mu="
+                                                f"{plist[s_].mu}, row={frow[s_]}", row=frow[s_], iteration=fit[s_])
+            h = hist[:S].cpu().numpy()
+            for s_ in range(len(group)):
+                n_it = int(its[s_])
+                xs = (x0 if n_it % 2 == 0 else x1)[s_].cpu().numpy()
                 A, B, C = (xs[k * n:(k + 1) * n].reshape(shape).copy() for k in range(3))
-                out_all.append(MuSolution(A=A, B=B, C=C, iterations=its[s_], converged=res[s_] is not None,
-                                          history=hist[s_], grid=grid, params=plist[s_]))
+                rec = [MuIterationRecord(0, float("nan"), float("nan"), float("nan"))]
+                rec += [MuIterationRecord(int(r[0]), float(r[1]), float(r[2]), float(r[3])) for r in h[s_, 1:n_it + 1]]
+                out_all.append(MuSolution(A=A, B=B, C=C, iterations=n_it, converged=bool(conv[s_]),
+                                          history=rec, grid=grid, params=plist[s_]))
     return out_all
 
 

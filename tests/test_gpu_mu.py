@@ -381,16 +381,18 @@ def test_device_anderson_kernels_match_numpy():
         assert np.max(np.abs(got - ref_x)) <= 1e-12 * np.max(np.abs(ref_x))
 
 
-@pytest.mark.parametrize("count", [3, 5])
-def test_batched_successive_approximation_equals_standalone(count):
-    """solve_mu_batch_sa (config 4's parity-equivalent path): each mu value's
-    iterations, history and state are bitwise its standalone solve_mu; groups
-    of 4 and a padded remainder."""
+@pytest.mark.parametrize("count,batch,cap", [(3, 4, 120), (5, 4, 120), (2, 2, 120), (5, 4, 7), (3, 2, 9)])
+def test_batched_successive_approximation_equals_standalone(count, batch, cap):
+    """solve_mu_batch_sa (config 4's parity-equivalent path, one cooperative
+    launch per group): each mu value's iterations, history and state are
+    bitwise its standalone solve_mu; groups of 4 and 2, a padded remainder,
+    and a cap below the convergence point (converged False, the capped
+    state)."""
     from paper_2012_03667_b200.finite_mu import solve_mu_batch_sa
-    p = MuParams(vertex="bcb", max_iterations=120, **SMALL)
+    p = MuParams(vertex="bcb", max_iterations=cap, **SMALL)
     g = grid_for(p)
     mus = [0.02 + 0.37 * k / count for k in range(count)]
-    batch = solve_mu_batch_sa(mus, p, g, batch=4)
+    batch = solve_mu_batch_sa(mus, p, g, batch=batch)
     assert len(batch) == count
     for m, sol in zip(mus, batch):
         one = solve_mu(MuParams(**{**p.__dict__, "mu": m}), g)
