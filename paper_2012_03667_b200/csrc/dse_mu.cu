@@ -866,6 +866,17 @@ struct MuBatch {
 #define DSE_MU_BATCH_SMACC 0  // per-thread accumulators of S = 4 in shared memory (frees 48 registers)
 #endif
 constexpr bool kBatchSmAcc = DSE_MU_BATCH_SMACC;
+#ifndef DSE_MU_BATCH_PF
+#define DSE_MU_BATCH_PF 2  // prefetch the next chunk's moments: 0 off, 1 into L1, 2 into L2 (S = 4 sweep 4.50 -> 4.42 ms)
+#endif
+constexpr int kBatchPf = DSE_MU_BATCH_PF;
+#ifndef DSE_MU_BATCH_PFNB
+#define DSE_MU_BATCH_PFNB 2  // also prefetch the next chunk's node values: 0 off, 1 always, 2 for S = 2 only
+#endif                       // (S = 2 2.56 -> 2.46 ms; S = 4 4.42 -> 4.46 ms, register pressure)
+template <int S>
+__host__ __device__ constexpr bool batch_pfnb() {
+    return DSE_MU_BATCH_PF && (DSE_MU_BATCH_PFNB == 1 || (DSE_MU_BATCH_PFNB == 2 && S == 2));
+}
 template <int S>
 __host__ __device__ constexpr size_t batch_acc_doubles() { return (kBatchSmAcc && S == 4) ? (size_t)S * 6 * kThreads : 0; }
 
@@ -915,7 +926,7 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_BATCH_MINB) mu_batch_kernel(M
             __syncthreads();
             if (r >= (unsigned)a.n_rows) break;
             const int i = a.row_start + (int)r * a.row_stride;
-            if (tid < S && (act >> tid & 1u)) {
+            if (tid < S) {  // every solve (a stopped one is contracted too, its sums unused: no branch in the pair loop)
                 MuArgs as = a;
                 as.mu = b.mu[tid];
                 as.coeff = b.coeff[tid];
@@ -934,17 +945,44 @@ __global__ void __launch_bounds__(kThreads, DSE_MU_BATCH_MINB) mu_batch_kernel(M
                     if (smacc) sacc[(s * 6 + c) * kThreads + tid] = 0.0;
                     else acc[smacc ? 0 : s][c] = 0.0;
                 }
+            constexpr bool kBatchPfNB = batch_pfnb<S>();
+            int jsn = 0, j4n = 0;  // this chunk's node (computed one chunk ahead when prefetching node values)
+            if (kBatchPfNB && total > 0) {
+                const int f = min(tid, total - 1);
+                jsn = node_of(roff, a.m_s, top, f);
+                j4n = rlo[jsn] + (f - roff[jsn]);
+            }
             for (int f0 = 0; f0 < total; f0 += kThreads) {
                 const int f = min(f0 + tid, total - 1);
-                const int js = node_of(roff, a.m_s, top, f);
-                const int j4 = rlo[js] + (f - roff[js]);
+                int js, j4;
+                if (kBatchPfNB) {
+                    js = jsn;
+                    j4 = j4n;
+                } else {
+                    js = node_of(roff, a.m_s, top, f);
+                    j4 = rlo[js] + (f - roff[js]);
+                }
                 DCHECK(total == 0 || (js >= 0 && js < a.m_s && j4 >= 0 && j4 < a.m_4), 24);
                 double mom[5];
                 for (int q = 0; q < 5; ++q) mom[q] = __ldcs(a.mo_mom + q * a.mo_stride + mbase + f);
+                if (kBatchPf && f0 + kThreads < total) {  // the next chunk's moments toward the SM (no registers held)
+                    const int fn = min(f0 + kThreads + tid, total - 1);
+                    for (int q = 0; q < 5; ++q) {
+                        const double* pa = a.mo_mom + q * a.mo_stride + mbase + fn;
+                        if (kBatchPf == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
+                        else asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
+                    }
+                    if (kBatchPfNB) {  // and its node values, every solve, into L1
+                        jsn = node_of(roff, a.m_s, top, fn);
+                        j4n = rlo[jsn] + (fn - roff[jsn]);
+                        for (int s = 0; s < S; ++s)
+                            asm volatile("prefetch.global.L1 [%0];" ::"l"(b.NB + (size_t)s * 4 * m_int +
+                                                                          4 * (size_t)(jsn * a.m_4 + j4n)));
+                    }
+                }
                 __syncwarp();
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
-                    if (!(act >> s & 1u)) continue;
                     const double2* nb = b.NB + (size_t)s * 4 * m_int + 4 * (size_t)(js * a.m_4 + j4);
                     const double2 vn[4] = {nb[0], nb[1], nb[2], nb[3]};
                     double part[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
