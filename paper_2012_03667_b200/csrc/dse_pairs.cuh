@@ -46,7 +46,10 @@ constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
 // (an int2 (row, group) item table instead of one int and a division ran
 // 0.350 vs 0.342 ms)
 // (requesting the next ticket while an item computes ran 0.353 vs 0.341 ms:
-// a busy warp then holds an item idle warps could run, the tail grows; angle
+// a busy warp then holds an item idle warps could run, the tail grows -- and
+// still 0.349 vs 0.341 ms in round 2 with the prefetch stopped 1, 2 or 4
+// grid-warps of items before the end; a multiply-high item -> row split
+// instead of the division measured no different, 0.342 ms; angle
 // chunks C = 2 / 4 at config 2 ran 0.362 / 0.410 ms: per-item overhead)
 // (two accumulator sets for even/odd angles ran 0.344 vs 0.339 ms: the loop
 // is FP64-pipe bound, not add-chain bound)

@@ -9,7 +9,8 @@ import paper_2012_03667_b200 as p  # noqa: E402
 
 out = {}
 rng = np.random.default_rng(11)
-v = p.VARIANTS["indexed-gpu-exact"]
+import os
+v = p.VARIANTS[os.environ.get("DSE_AB_VARIANT", "indexed-gpu-exact")]
 for (n, m, k) in ((128, 128, 64), (1024, 1024, 256), (150, 100, 32), (37, 29, 5), (2, 2, 1), (256, 256, 256)):
     g = p.build_grid(n, m, k, 1e-6, 1e4)
     for si, (a, b) in enumerate([(np.ones(n), np.full(n, 0.3)), (rng.uniform(0.8, 2.5, n), rng.uniform(0, 1.6, n)),
