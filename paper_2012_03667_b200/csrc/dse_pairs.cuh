@@ -55,6 +55,14 @@ constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
 // is FP64-pipe bound, not add-chain bound)
 // (an 11-bit exp table with a degree-3 polynomial ran 0.333 ms but put a
 // config-2 random-state sweep at 1.1e-12 of the oracle: kept at 8 bits, degree 4)
+// (mirror pairs, round 2: the angular nodes are symmetric to ~3e-16, so
+// nodes k and K-1-k could share one rz from the positive node (kappa's
+// cancelling side stays exact) and the moments fold to (t0+ -/+ t0-) etc.:
+// 21 instead of 23 FP64 per point, 0.341 -> 0.319 ms -- but the borrowed rz
+// perturbs every negative-side kappa by the SAME node asymmetry in every
+// row, a coherent bias that the B channel's cancelling sums amplify: a
+// config-2 random-state sweep went from 4.3e-13 to 8.3e-13 of the oracle,
+// past the 5e-13 bar.  Not kept.)
 // (fewer accumulators: with r = (psum - kappa)/2 and rho kappa = 1, T1 =
 // (psum T0 - S0)/2, T2 = (psum T1 - S1)/2, even S1 = (psum S0 - sum ew)/2 --
 // 3 to 4 FP64 instructions fewer per point, but a numpy model against long
