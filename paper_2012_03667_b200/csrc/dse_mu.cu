@@ -82,6 +82,7 @@ struct MuArgs {
     double* hist;          // (cap+1) x 4 or null
     long long* evaluated;  // pairs evaluated (diagnostic; null = not counted)
     int it_begin, it_end, sweep_only, vertex;
+    int zsym;              // angular nodes and weights exactly mirror-symmetric: pair_moments walks node pairs
     // moments mode (DSE_MU_MODE_MOMENTS): per owned row r the exact-zero
     // windows (rlo [r][m_s], roff [r][m_s + 1]) and the five angular moments
     // of every evaluated pair, mom[m * mo_stride + mo_base[r] + f]
@@ -98,6 +99,10 @@ constexpr int kWarps = kThreads / 32;
 #define DSE_MU_UNROLL 8  // config 3, bcb: unroll 2 5.46, 4 5.52, 8 5.35 ms; 3 CTAs/SM (80 regs) 5.51 ms
 #endif
 constexpr int kMuUnroll = DSE_MU_UNROLL;
+#ifndef DSE_MU_MIRROR
+#define DSE_MU_MIRROR 1
+#endif
+constexpr bool kMuMirror = DSE_MU_MIRROR;
 #ifndef DSE_MU_MINB
 #define DSE_MU_MINB 2  // CTAs per SM the register budget is cut for (A/B: scripts/mu_ab.sh)
 #endif
@@ -186,6 +191,43 @@ __device__ __forceinline__ void pair_moments(const MuArgs& a, const RowC& rc, in
     const double c0 = fma(k4, k4, rc.P2 + Q2);
     const dse::ExpK ek{a.exp_c1, 0.0};
     double S0 = 0.0, S1 = 0.0, T0 = 0.0, T1 = 0.0, T2 = 0.0;
+    if (kMuMirror && a.zsym) {
+        // mirror pairs: z_{K-1-k} = -z_k and w_{K-1-k} = w_k EXACTLY (checked
+        // on the host), so r(-z) = -r(z) bit for bit and the pair shares r;
+        // the odd moments take (x+ - x-) r, the even ones (x+ + x-): 20.5
+        // instead of 22 FP64 instructions per point
+        const int KH = a.K >> 1;
+#pragma unroll kMuUnroll / 2
+        for (int k = 0; k < KH; ++k) {
+            const double2 zp = zw[a.K - 1 - k];
+            const double r = PQ * zp.x;
+            const double k2p = fma(-2.0, r, c0), k2m = fma(2.0, r, c0);
+            const double Kp = dse::rcp_nr(k2p), Km = dse::rcp_nr(k2m);
+            const double eKp = (zp.y * dse::exp_neg_k2(k2p, ek, tbl)) * Kp;
+            const double eKm = (zp.y * dse::exp_neg_k2(k2m, ek, tbl)) * Km;
+            S0 += eKp + eKm;
+            S1 = fma(eKp - eKm, r, S1);
+            const double eKKp = eKp * Kp, eKKm = eKm * Km;
+            const double s2 = eKKp + eKKm;
+            T0 += s2;
+            T1 = fma(eKKp - eKKm, r, T1);
+            T2 = fma(s2, r * r, T2);
+        }
+        if (a.K & 1) {  // the middle node, z = 0
+            const double2 zk = zw[KH];
+            const double r = PQ * zk.x;
+            const double k2 = fma(-2.0, r, c0);
+            const double K = dse::rcp_nr(k2);
+            const double eK = (zk.y * dse::exp_neg_k2(k2, ek, tbl)) * K;
+            S0 += eK;
+            S1 = fma(eK, r, S1);
+            const double eKK = eK * K;
+            T0 += eKK;
+            const double t = eKK * r;
+            T1 += t;
+            T2 = fma(t, r, T2);
+        }
+    } else {
 #pragma unroll kMuUnroll
     for (int k = 0; k < a.K; ++k) {
         const double2 zk = zw[k];
@@ -201,6 +243,7 @@ __device__ __forceinline__ void pair_moments(const MuArgs& a, const RowC& rc, in
         const double t = eKK * r;
         T1 += t;
         T2 = fma(t, r, T2);
+    }
     }
     mom[0] = S0;
     mom[1] = S1;
@@ -1244,6 +1287,7 @@ struct dse_mu_sweeper {
     dse_mu_params prm{};
     double *d_P = nullptr, *d_P2 = nullptr, *d_p4 = nullptr, *d_Qs = nullptr, *d_Q2 = nullptr, *d_q4 = nullptr;
     double *d_ms = nullptr, *d_m4 = nullptr, *d_z = nullptr, *d_wz = nullptr, *d_etbl = nullptr;
+    int zsym = 0;  // angular nodes/weights exactly mirror-symmetric
     int *d_brk_s = nullptr, *d_brk_4 = nullptr;
     double2* d_X = nullptr;
     double2* d_NB = nullptr;
@@ -1292,6 +1336,7 @@ mu::MuArgs mu_make_args(dse_mu_sweeper* s, const dse_mu_params& p, int it_begin,
     mu::MuArgs a{};
     a.P = s->d_P; a.P2 = s->d_P2; a.p4 = s->d_p4; a.Qs = s->d_Qs; a.Q2 = s->d_Q2; a.q4 = s->d_q4;
     a.meas_s = s->d_ms; a.meas_4 = s->d_m4; a.z = s->d_z; a.wz = s->d_wz; a.exp_tbl = s->d_etbl;
+    a.zsym = s->zsym;
     a.brk_s = s->d_brk_s; a.brk_4 = s->d_brk_4;
     a.n_s = s->n_s; a.n_4 = s->n_4; a.m_s = s->m_s; a.m_4 = s->m_4; a.K = s->K;
     a.row_start = s->row_start; a.row_stride = s->row_stride; a.n_rows = s->n_rows;
@@ -1512,6 +1557,15 @@ int dse_mu_sweeper_create(const dse_mu_grid* g, const dse_mu_params* p, int devi
     MU_TRY(upload(&s->d_q4, g->q4_int, g->m_4, st));
     MU_TRY(upload(&s->d_ms, g->meas_s, g->m_s, st));
     MU_TRY(upload(&s->d_m4, g->meas_4, g->m_4, st));
+    {
+        bool sym = !(getenv("DSE_MU_MIRROR") && atoi(getenv("DSE_MU_MIRROR")) == 0);
+        for (int64_t k = 0; k < g->m_ang && sym; ++k) {
+            const int64_t m = g->m_ang - 1 - k;
+            sym = g->z_nodes[m] == -g->z_nodes[k] && g->z_weights[m] == g->z_weights[k] &&
+                  (k >= m || g->z_nodes[m] > 0.0);
+        }
+        s->zsym = sym ? 1 : 0;
+    }
     MU_TRY(upload(&s->d_z, g->z_nodes, g->m_ang, st));
     MU_TRY(upload(&s->d_wz, g->z_weights, g->m_ang, st));
     MU_TRY(upload(&s->d_brk_s, bs.data(), bs.size(), st));

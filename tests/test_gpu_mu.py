@@ -207,7 +207,9 @@ def test_sharded_iteration_world3_emulated():
         for f in range(3):
             assert np.array_equal(full[f].view(np.float64), ref[f].view(np.float64))
         d = delta.cpu().numpy()
-        assert d[0] == np.max(np.abs(ref[0] - A))
+        # |new - old| is CUDA's hypot on the device, numpy's here: the two
+        # libraries may differ by an ulp (the state itself is compared bitwise)
+        np.testing.assert_allclose(d, [np.max(np.abs(r - x)) for r, x in zip(ref, (A, B, C))], rtol=4.5e-16, atol=0)
     for sw in sws:
         sw.close()
 
