@@ -606,8 +606,9 @@ def interp_bench(p, nat, torch, dev, hbm):
     return res
 
 
-# ncu SASS mix of mu_solve_kernel<bcb> (profiles/r01/mu_sweep.md, final round-1 build): 2*DFMA + DMUL + DADD per evaluated point
-MU_FLOP_PER_POINT = 42.57
+# ncu SASS mix of mu_solve_kernel<bcb> (profiles/r02/mu_sweep_r02.md, mirror-pair build): 2*DFMA + DMUL + DADD
+# per evaluated point (2 x 15.06 + 6.59 + 4.33; 42.57 before the mirror pairs)
+MU_FLOP_PER_POINT = 41.04
 
 
 def mu_cpu_rate(budget_s: float):
