@@ -184,6 +184,14 @@ class IterationRecord:
     probe_b: tuple[float, ...]
 
 
+def _records(hist: np.ndarray, P: int) -> list:
+    """History rows (n, |dA|, |dB|, P probes of A, P of B) -> IterationRecords
+    (one tolist() instead of a float() per element: ~3x faster for the long
+    histories of batched scans)."""
+    return [IterationRecord(int(r[0]), r[1], r[2], tuple(r[3:3 + P]), tuple(r[3 + P:3 + 2 * P]))
+            for r in hist.tolist()]
+
+
 @dataclass
 class PropagatorSolution:
     A: np.ndarray
@@ -489,8 +497,7 @@ def solve(params: ModelParams, variant: AlgorithmVariant, grid: MomentumGrid | N
         sweeper = _make_sweeper(grid, params, variant)
         a, b, n, conv, hist = sweeper.solve(a, b, probes_p2)
     P = len(probes_p2)
-    history = [IterationRecord(int(r[0]), float(r[1]), float(r[2]), tuple(float(x) for x in r[3:3 + P]),
-                               tuple(float(x) for x in r[3 + P:3 + 2 * P])) for r in hist]
+    history = _records(hist, P)
     return PropagatorSolution(A=a, B=b, iterations=n, converged=conv, history=history, grid=grid,
                               params=params, probes_log10p=tuple(probes_log10p))
 
@@ -525,7 +532,7 @@ def solve_batch(params_list, variant: AlgorithmVariant, grid: MomentumGrid | Non
     P = probes_p2.size
     W = 3 + 2 * P
     cap_max = max(int(p.max_iterations) for p in params_list)
-    hist = np.full((S, cap_max + 1, W), np.nan)
+    hist = np.empty((S, cap_max + 1, W))  # rows 0..iterations of each solve are written by the library
     keep = [nat.as_f64(grid.p2_ext), nat.as_f64(grid.q2_int), nat.as_f64(grid.sqrt_q2_int),
             nat.as_f64(grid.radial_measure), nat.as_i64(grid.bracket_idx), nat.as_f64(grid.z_nodes),
             nat.as_f64(grid.z_weights)]
@@ -548,9 +555,7 @@ def solve_batch(params_list, variant: AlgorithmVariant, grid: MomentumGrid | Non
     out = []
     for k, prm in enumerate(params_list):
         nk = int(its[k])
-        h = hist[k, : nk + 1]
-        records = [IterationRecord(int(r[0]), float(r[1]), float(r[2]), tuple(float(x) for x in r[3:3 + P]),
-                                   tuple(float(x) for x in r[3 + P:3 + 2 * P])) for r in h]
+        records = _records(hist[k, : nk + 1], P)
         out.append(PropagatorSolution(A=A[k].copy(), B=B[k].copy(), iterations=nk, converged=bool(conv[k]),
                                       history=records, grid=grid, params=prm, probes_log10p=tuple(probes_log10p)))
     return out

@@ -28,7 +28,7 @@ def batch_mode(request, monkeypatch):
     return request.param
 
 
-@pytest.mark.parametrize("vname", ["indexed-gpu", "search-gpu-exact"])
+@pytest.mark.parametrize("vname", ["indexed-gpu", "search-gpu-exact", "indexed-gpu-moments", "search-gpu-moments"])
 def test_batch_equals_individual_solves(vname, batch_mode):
     g = golden_grid("default")
     plist = [params_ns(D=d, m0=m0, relaxation=r, xi=1e-6, max_iterations=cap)
@@ -42,14 +42,15 @@ def test_batch_equals_individual_solves(vname, batch_mode):
     assert batch[4].iterations == 3 and not batch[4].converged       # cap
 
 
-def test_batch_config0_scan(batch_mode):
+@pytest.mark.parametrize("vname", ["indexed-gpu", "indexed-gpu-moments"])
+def test_batch_config0_scan(batch_mode, vname):
     z = golden("solve_c0.npz")
     g = golden_grid("c0")
     plist = [params_ns(D=d, xi=1e-10, max_iterations=4000) for d in (0.55, 0.5, 0.6)]
-    sols = p.solve_batch(plist, p.VARIANTS["indexed-gpu"], grid=g, b0s=np.full((3, g.n_ext), 0.3))
+    sols = p.solve_batch(plist, p.VARIANTS[vname], grid=g, b0s=np.full((3, g.n_ext), 0.3))
     assert sols[0].iterations == int(z["iterations"]) == 2923 and sols[0].converged
     for prm, got in zip(plist[1:], sols[1:]):
-        _same(got, p.solve(prm, p.VARIANTS["indexed-gpu"], grid=g, b0=np.full(g.n_ext, 0.3)))
+        _same(got, p.solve(prm, p.VARIANTS[vname], grid=g, b0=np.full(g.n_ext, 0.3)))
 
 
 def test_batch_validation():
@@ -58,16 +59,17 @@ def test_batch_validation():
     assert p.solve_batch([], p.VARIANTS["indexed-gpu"]) == []
 
 
-def test_batch_failure_is_per_solve_and_located(batch_mode):
+@pytest.mark.parametrize("vname", ["indexed-gpu", "indexed-gpu-moments"])
+def test_batch_failure_is_per_solve_and_located(batch_mode, vname):
     g = golden_grid("small")
     b0s = np.full((2, g.n_ext), 0.3)
     a0s = np.ones((2, g.n_ext))
     a0s[1, 5] = np.inf
     with pytest.raises(p.NumericalFailureError) as ei:
-        p.solve_batch([params_ns(xi=1e-3, max_iterations=5)] * 2, p.VARIANTS["indexed-gpu"], grid=g, a0s=a0s, b0s=b0s)
+        p.solve_batch([params_ns(xi=1e-3, max_iterations=5)] * 2, p.VARIANTS[vname], grid=g, a0s=a0s, b0s=b0s)
     single = None
     try:
-        p.solve(params_ns(xi=1e-3, max_iterations=5), p.VARIANTS["indexed-gpu"], grid=g, a0=a0s[1], b0=b0s[1])
+        p.solve(params_ns(xi=1e-3, max_iterations=5), p.VARIANTS[vname], grid=g, a0=a0s[1], b0=b0s[1])
     except p.NumericalFailureError as exc:
         single = exc
     assert single is not None
