@@ -74,3 +74,18 @@ def test_batch_failure_is_per_solve_and_located(batch_mode, vname):
         single = exc
     assert single is not None
     assert (ei.value.row, ei.value.radial, ei.value.angular) == (single.row, single.radial, single.angular)
+
+
+def test_batch_moments_mixed_omega_falls_back_bitwise():
+    """Moments solves with different omegas cannot share one moment table:
+    solve_batch runs them on the per-solve path, still bitwise the standalone
+    solves."""
+    g = golden_grid("default")
+    plist = [params_ns(D=0.55, omega=0.678, xi=1e-6, max_iterations=200),
+             params_ns(D=0.55, omega=0.6, xi=1e-6, max_iterations=200),
+             params_ns(D=0.5, omega=0.678, xi=1e-6, max_iterations=200)]
+    v = p.VARIANTS["indexed-gpu-moments"]
+    b0s = np.full((3, g.n_ext), 0.3)
+    batch = p.solve_batch(plist, v, grid=g, b0s=b0s)
+    for prm, b0, got in zip(plist, b0s, batch):
+        _same(got, p.solve(prm, v, grid=g, b0=b0))
