@@ -69,3 +69,25 @@ def test_multi_gpu_without_torchrun_is_a_parameter_error(monkeypatch):
     prm = p.ModelParams(N=8, m_rad=6, m_ang=2)
     with pytest.raises((p.ParameterError, p.ExecutionEnvironmentError)):
         p.iterate_once(g, np.ones(8), np.ones(8), prm, p.VARIANTS["indexed-gpu-pairs"].with_gpus(2))
+
+
+def test_history_records_conversion():
+    """solver._records (one tolist() per history) builds exactly the
+    IterationRecords the per-element float() form did, NaN row 0 included."""
+    import numpy as np
+    from paper_2012_03667_b200.solver import IterationRecord, _records
+    rng = np.random.default_rng(3)
+    for P in (0, 1, 2, 5):
+        h = rng.standard_normal((17, 3 + 2 * P))
+        h[:, 0] = np.arange(17)
+        h[0, 1:3] = np.nan
+        old = [IterationRecord(int(r[0]), float(r[1]), float(r[2]), tuple(float(x) for x in r[3:3 + P]),
+                               tuple(float(x) for x in r[3 + P:3 + 2 * P])) for r in h]
+        new = _records(h, P)
+        assert len(new) == len(old)
+        for a, b in zip(new, old):
+            assert a.iteration == b.iteration and type(a.iteration) is int
+            assert np.array_equal(np.array([a.max_delta_a, a.max_delta_b]), np.array([b.max_delta_a, b.max_delta_b]),
+                                  equal_nan=True)
+            assert a.probe_a == b.probe_a and a.probe_b == b.probe_b
+            assert all(type(x) is float for x in a.probe_a + a.probe_b)
