@@ -730,7 +730,7 @@ def bench_main(args, metric, unit, cfg, flop_per_point):
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": None,
                          "flop_per_point": flop_per_point, "points": "evaluated, per GPU",
-                         "peak_source": "measured: dse_fp64_peak DFMA probe (per GPU)"},
+                         "peak_source": "builder-measured: dse_fp64_peak DFMA probe, in process, per GPU (MEASURED_PEAKS.json has no fp64 figure)"},
             "gpu_launches": launches,
             "per_rank_ms_per_step": per_rank_ms,
             "clocks": clk.summary() if clk is not None else None,
