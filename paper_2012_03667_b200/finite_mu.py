@@ -577,14 +577,22 @@ def owned_mus(mus, rank: int, world: int) -> list:
 def solve_mu_batch_sharded(mus, params: MuParams | None = None, grid: MuGrid | None = None, device: int = 0,
                            rank: int | None = None, world: int | None = None) -> list:
     """BASELINE config 4 across the ranks of a torch.distributed job (one
-    process per GPU): rank r solves owned_mus(mus, r, W) on its GPU, then the
-    (mu, iterations, converged, A, B, C) records are all-gathered so every
-    rank returns the full list in the order of `mus`."""
+    process per GPU): rank r solves owned_mus(mus, r, W) on its GPU -- by
+    solve_mu_batch_sa (4 mu values per cooperative launch, one moment table
+    per rank; bitwise the standalone solves) when the relaxation is 1, else
+    one by one -- then the (mu, iterations, converged, A, B, C) records are
+    all-gathered so every rank returns the full list in the order of `mus`."""
     import torch.distributed as dist
     if rank is None or world is None:
         rank, world = dist.get_rank(), dist.get_world_size()
     mine = owned_mus(mus, rank, world)
-    sols = solve_mu_batch(mine, params, grid, device)
+    prm = MuParams() if params is None else params
+    if not mine:
+        sols = []
+    elif prm.relaxation == 1.0:
+        sols = solve_mu_batch_sa(mine, prm, grid, batch=4 if len(mine) > 2 else 2, device=device)
+    else:
+        sols = solve_mu_batch(mine, prm, grid, device)
     recs = [(float(m), s.iterations, s.converged, s.A, s.B, s.C) for m, s in zip(mine, sols)]
     if world == 1:
         gathered = [recs]

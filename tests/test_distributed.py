@@ -120,6 +120,10 @@ def _run_mu(rank, world, port, q):
                                       A=np.full(2, m), B=np.full(2, 2 * m), C=np.full(2, 3 * m)) for m in mus]
 
     finite_mu.solve_mu_batch = fake_batch
+
+    def fake_batch_sa(mus, params=None, grid=None, batch=4, device=0):
+        return fake_batch(mus, params, grid, device)
+    finite_mu.solve_mu_batch_sa = fake_batch_sa
     mus = [0.4 * (k + 0.5) / 32 for k in range(32)]
     recs = finite_mu.solve_mu_batch_sharded(mus, grid=object())
     q.put((rank, [(r[0], r[1], float(r[3][0])) for r in recs]))

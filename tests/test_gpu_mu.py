@@ -404,3 +404,19 @@ def test_batched_successive_approximation_equals_standalone(count, batch, cap):
         h1 = [(r.n, r.delta_a, r.delta_b, r.delta_c) for r in one.history]
         h2 = [(r.n, r.delta_a, r.delta_b, r.delta_c) for r in sol.history]
         assert np.array_equal(np.array(h1[1:]), np.array(h2[1:]))
+
+
+def test_batch_sharded_world1_equals_standalone():
+    """solve_mu_batch_sharded (config 4's public multi-GPU API) at world 1:
+    the batched successive approximation path, every record bitwise the
+    standalone solve_mu."""
+    from paper_2012_03667_b200.finite_mu import solve_mu_batch_sharded
+    p = MuParams(vertex="bcb", max_iterations=120, **SMALL)
+    g = grid_for(p)
+    mus = [0.05, 0.15, 0.25, 0.35, 0.3]
+    recs = solve_mu_batch_sharded(mus, p, g, rank=0, world=1)
+    for m, (mu_r, its, conv, A, B, C) in zip(mus, recs):
+        one = solve_mu(MuParams(**{**p.__dict__, "mu": m}), g)
+        assert mu_r == m and its == one.iterations and conv == one.converged
+        for x, y in ((A, one.A), (B, one.B), (C, one.C)):
+            assert np.array_equal(x.view(np.float64), y.view(np.float64))
