@@ -1,0 +1,57 @@
+"""Randomised parity sweep (GPU vs the C oracle): random grid shapes, states
+and parameters through iterate_once for every arithmetic, and short solves
+compared on iteration counts.  Prints one JSON line per failure and a summary.
+Usage: python scripts/fuzz_sweeps.py [cases] [seed]"""
+import json, sys
+sys.path.insert(0, "."); sys.path.insert(0, "oracle")
+import numpy as np
+import oracle
+import paper_2012_03667_b200 as p
+
+def hybrid_rel(x, ref, floor=1e-6):
+    m = float(np.max(np.abs(ref)))
+    if m == 0.0:
+        return float(np.max(np.abs(x - ref)))
+    big = np.abs(ref) >= floor * m
+    err = np.abs(x - ref)
+    return float(np.max(np.where(big, err / np.where(big, np.abs(ref), 1.0), err / m)))
+
+cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
+TOL = {"exact": 1e-13, "fast": 5e-13, "pairs": 5e-13, "moments": 5e-13}
+VAR = {"exact": "indexed-gpu-exact", "fast": "indexed-gpu", "pairs": "indexed-gpu-pairs", "moments": "indexed-gpu-moments"}
+worst = {k: 0.0 for k in TOL}
+fails = 0
+for c in range(cases):
+    N = int(rng.integers(2, 400)); M = int(rng.integers(2, 400)); K = int(rng.integers(1, 90))
+    g = p.build_grid(N, M, K, 10.0 ** rng.uniform(-7, -3), 10.0 ** rng.uniform(2, 5))
+    prm = p.ModelParams(N=N, m_rad=M, m_ang=K, D=float(rng.uniform(0.1, 1.2)), omega=float(rng.uniform(0.3, 1.0)),
+                        m0=float(rng.choice([0.0, 0.005, 0.1])), z1=float(rng.uniform(0.8, 1.2)))
+    kind = c % 4
+    a = rng.uniform(0.7, 3.0, N)
+    b = rng.uniform(0.0, 2.0, N)
+    if kind == 1:
+        b = b * 10.0 ** rng.uniform(-250, 0, N)     # UV-tail-like tiny B
+    elif kind == 2:
+        b = np.zeros(N)                             # chiral
+    ra, rb = oracle.sweep(g, a, b, prm, strategy=1, threads=oracle.max_threads())
+    for ar, vname in VAR.items():
+        try:
+            ga, gb = p.iterate_once(g, a, b, prm, p.VARIANTS[vname])
+        except p.NumericalFailureError as exc:
+            print(json.dumps({"case": c, "arith": ar, "gpu_failure": str(exc)[:80]})); fails += 1; continue
+        e = max(hybrid_rel(ga, ra), hybrid_rel(gb, rb))
+        worst[ar] = max(worst[ar], e)
+        if not e <= TOL[ar]:
+            fails += 1
+            print(json.dumps({"case": c, "arith": ar, "N": N, "M": M, "K": K, "kind": kind, "err": e}))
+    if c % 6 == 0 and N * M * K <= 2_000_000:   # a short solve: iteration counts equal
+        sp = p.ModelParams(N=N, m_rad=M, m_ang=K, D=prm.D, omega=prm.omega, m0=prm.m0, z1=prm.z1, xi=1e-8,
+                           max_iterations=400)
+        _, _, n, conv, _ = oracle.solve(g, sp, np.ones(N), np.full(N, 0.3), strategy=1, threads=oracle.max_threads())
+        for ar in ("exact", "moments"):
+            sol = p.solve(sp, p.VARIANTS[VAR[ar]], grid=g, b0=np.full(N, 0.3))
+            if sol.iterations != n or sol.converged != conv:
+                fails += 1
+                print(json.dumps({"case": c, "solve": ar, "gpu": sol.iterations, "oracle": n}))
+print(json.dumps({"cases": cases, "failures": fails, "worst": worst}))
