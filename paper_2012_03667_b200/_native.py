@@ -134,6 +134,8 @@ _PROTOS = [
                                             ctypes.POINTER(DseErr)]),
     ("dse_debug_exp_exact", ctypes.c_int, [ctypes.c_int, f64p, ctypes.c_int64, f64p, f64p, i32p,
                                            ctypes.POINTER(DseErr)]),
+    ("dse_debug_qdiv_ext", ctypes.c_int, [ctypes.c_int, f64p, f64p, ctypes.c_int64, f64p, f64p, i32p,
+                                          ctypes.POINTER(DseErr)]),
     ("dse_plan_info", ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, i32p, i32p, ctypes.c_int64, i32p, i32p, i32p,
                                      ctypes.c_int64, i64p, i64p]),
     ("dse_debug_check_flags", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32)]),
@@ -283,6 +285,20 @@ def debug_exp_exact(x, device: int = 0):
                                     e.ctypes.data_as(f64p), k.ctypes.data_as(i32p), _ct.byref(err))
     raise_for(rc, err)
     return r, e, k.astype(bool)
+
+
+def debug_qdiv_ext(a, b, device: int = 0):
+    """Test hook (dse_debug_qdiv_ext): (qdiv_ext, __ddiv_rn, ext valid) of a / b."""
+    import ctypes as _ct
+    va = np.ascontiguousarray(a, dtype=np.float64)
+    vb = np.ascontiguousarray(b, dtype=np.float64)
+    e, r, k = np.empty(va.size), np.empty(va.size), np.empty(va.size, dtype=np.int32)
+    err = DseErr()
+    rc = load().dse_debug_qdiv_ext(device, va.ctypes.data_as(f64p), vb.ctypes.data_as(f64p), va.size,
+                                   e.ctypes.data_as(f64p), r.ctypes.data_as(f64p), k.ctypes.data_as(i32p),
+                                   _ct.byref(err))
+    raise_for(rc, err)
+    return e, r, k.astype(bool)
 
 
 def plan_info(n: int, chunk_leaves: int = 1 << 30):
