@@ -50,7 +50,10 @@ constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
 // still 0.349 vs 0.341 ms in round 2 with the prefetch stopped 1, 2 or 4
 // grid-warps of items before the end; a multiply-high item -> row split
 // instead of the division measured no different, 0.342 ms; angle
-// chunks C = 2 / 4 at config 2 ran 0.362 / 0.410 ms: per-item overhead)
+// chunks C = 2 / 4 at config 2 ran 0.362 / 0.410 ms: per-item overhead;
+// round 2, third session: the next ticket requested only after the angular
+// loop, its round trip overlapping the reduction and completion fences, ran
+// 0.347 vs 0.341 ms, bitwise equal)
 // (two accumulator sets for even/odd angles ran 0.344 vs 0.339 ms: the loop
 // is FP64-pipe bound, not add-chain bound)
 // (an 11-bit exp table with a degree-3 polynomial ran 0.333 ms but put a

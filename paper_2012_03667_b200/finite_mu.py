@@ -26,7 +26,7 @@ from .errors import NumericalFailureError, ParameterError
 from .mu_grid import MODES, VERTICES, MuGrid, MuParams, build_mu_grid, grid_for
 
 __all__ = ["MuIterationRecord", "MuSolution", "MuSweeper", "solve_mu", "iterate_mu_once", "solve_mu_batch",
-           "solve_mu_batch_sharded", "solve_mu_sharded", "solve_mu_anderson", "solve_mu_batch_anderson", "owned_mus", "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
+           "solve_mu_batch_sharded", "solve_mu_sharded", "solve_mu_anderson", "solve_mu_batch_anderson", "solve_mu_newton", "NewtonReport", "owned_mus", "interp_mu", "MuParams", "MuGrid", "build_mu_grid"]
 
 
 @dataclass(frozen=True)
@@ -604,6 +604,178 @@ def solve_mu_batch_sharded(mus, params: MuParams | None = None, grid: MuGrid | N
         for r in part:
             by_mu[r[0]] = r
     return [by_mu[float(m)] for m in mus]
+
+
+@dataclass
+class NewtonReport:
+    """Per-solve record of solve_mu_newton: sweeps used by the start solve
+    and by the Newton steps, and per Newton step (residual max per function,
+    GMRES iterations)."""
+    start_iterations: int
+    sweeps: int
+    steps: list = field(default_factory=list)   # (step, max|F_A|, max|F_B|, max|F_C|, gmres_iterations)
+
+
+def _gmres_real(matvec, b, rtol: float, restart: int, max_restarts: int, dot):
+    """Restarted GMRES for J dx = b in the REAL inner product Re<u, v> of the
+    complex state (the sweep is not holomorphic in (A, B, C) in general, so
+    J is a real-linear map of the 2n real components).  Classical Gram-
+    Schmidt applied twice (one stacked product per pass); the small
+    Hessenberg least-squares problem is solved on the host."""
+    import torch
+    x = torch.zeros_like(b)
+    bnorm = float(dot(b, b)) ** 0.5
+    if bnorm == 0.0:
+        return x, 0
+    total = 0
+    r = b.clone()
+    for _ in range(max_restarts):
+        beta = float(dot(r, r)) ** 0.5
+        if beta <= rtol * bnorm:
+            break
+        V = torch.zeros((restart + 1, b.numel()), dtype=b.dtype, device=b.device)
+        H = np.zeros((restart + 1, restart))
+        V[0] = r / beta
+        k_used = 0
+        y = np.zeros(0)
+        for k in range(restart):
+            w = matvec(V[k])
+            total += 1
+            for _pass in range(2):
+                h = torch.real(torch.conj(V[:k + 1]) @ w)
+                w = w - (h.to(V.dtype)[:, None] * V[:k + 1]).sum(0)
+                H[:k + 1, k] += h.cpu().numpy()
+            H[k + 1, k] = float(dot(w, w)) ** 0.5
+            k_used = k + 1
+            e1 = np.zeros(k + 2)
+            e1[0] = beta
+            y, *_ = np.linalg.lstsq(H[:k + 2, :k + 1], e1, rcond=None)
+            res = np.linalg.norm(H[:k + 2, :k + 1] @ y - e1)
+            if H[k + 1, k] == 0.0 or res <= rtol * bnorm:
+                break
+            V[k + 1] = w / H[k + 1, k]
+        x = x + (torch.from_numpy(y).to(V.device).to(V.dtype)[:, None] * V[:k_used]).sum(0)
+        r = b - matvec(x)
+        total += 1
+        if float(dot(r, r)) ** 0.5 <= rtol * bnorm:
+            break
+    return x, total
+
+
+def solve_mu_newton(params: MuParams | None = None, grid: MuGrid | None = None, a0=None, b0=None, c0=None,
+                    start: str | None = "bcb", max_newton: int = 40, restart: int = 60, max_restarts: int = 4,
+                    fd_eps: float = 1e-7, line_search: int = 0, device: int = 0,
+                    sweeper: "MuSweeper | None" = None):
+    """Finite-mu solve by Newton-Krylov on the fixed-point residual
+    F(x) = g(x) - x, g = one Jacobi sweep (the device sweep of solve_mu),
+    x = (A, B, C) complex: each Newton step solves J dx = -F with restarted
+    GMRES in the real inner product, every Jacobian-vector product one
+    forward difference of the sweep, (g(x + h v) - g(x)) / h - v with
+    h = fd_eps (1 + |x|) / |v|; inexact-Newton forcing term
+    min(0.1, max(1e-4, max|F|)); line_search > 0 backtracks (halving, at
+    most that many extra sweeps) while |F|_2 grows.  Stops when max|F| of A, B and C are all
+    < xi (the successive-approximation rule applied to the sweep's update,
+    as solve_mu_anderson).
+
+    This is the solver for the FULL in-medium Ball-Chiu vertex ('bc'):
+    successive approximation, relaxation and Anderson acceleration all
+    diverge on it (the sweep's Jacobian has eigenvalues far outside the unit
+    circle), Newton's method does not need a contraction.  By
+    default (start='bcb') the initial guess is the converged solve of the
+    same parameters with the 'bcb' vertex (plain successive approximation
+    on the device); start=None starts from (a0, b0, c0).  Not
+    iteration-equivalent to anything in the reference (which has no finite-mu
+    path).  Returns (MuSolution, NewtonReport); the solution's `iterations`
+    counts Newton steps and its history rows hold max|F| per function after
+    each step."""
+    import torch
+    params = MuParams() if params is None else params
+    params.validate()
+    grid = grid_for(params) if grid is None else grid
+    _check_c_projection(grid, params)
+    dev = torch.device("cuda", device)
+    n = grid.n_ext
+    shape = (grid.n_s, grid.n_4)
+    lib = nat.load()
+    own = sweeper is None
+    sw = MuSweeper(grid, params, device) if own else sweeper
+    start_its = 0
+    try:
+        if start is not None:
+            s0 = sw.solve(replace(params, vertex=start), a0, b0, c0, history=False)
+            if not s0.converged:
+                raise NumericalFailureError(f"start solve ({start}) did not converge in {params.max_iterations}")
+            start_its = s0.iterations
+            a0, b0, c0 = s0.A, s0.B, s0.C
+        x = torch.cat([torch.from_numpy(_state(v, shape, d).reshape(-1)) for v, d in ((a0, 1.0), (b0, 0.3),
+                                                                                         (c0, 1.0))]).to(dev)
+        gx = torch.zeros_like(x)
+        cp = _c_params(params)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        err = nat.DseErr()
+        sweeps = [0]
+
+        def g(v, out):
+            nat.raise_for(lib.dse_mu_solve_load(sw.handle, v[:n].data_ptr(), v[n:2 * n].data_ptr(),
+                                                v[2 * n:].data_ptr(), st, ctypes.byref(err)), err)
+            nat.raise_for(lib.dse_mu_sharded_sweep_pack(sw.handle, ctypes.byref(cp), out.data_ptr(), n, st,
+                                                        ctypes.byref(err)), err)
+            nat.raise_for(lib.dse_mu_sharded_failure(sw.handle, st, ctypes.byref(err)), err)
+            sweeps[0] += 1
+            return out
+
+        def dot(u, v):
+            return torch.real(torch.vdot(u, v)).item()
+
+        report = NewtonReport(start_iterations=start_its, sweeps=0)
+        hist = [MuIterationRecord(0, float("nan"), float("nan"), float("nan"))]
+        converged, step = False, 0
+        gp = torch.zeros_like(x)
+        for step in range(1, max_newton + 2):
+            g(x, gx)
+            F = gx - x
+            d = torch.stack([F[k * n:(k + 1) * n].abs().max() for k in range(3)]).cpu().numpy()
+            if step > 1:
+                hist.append(MuIterationRecord(step - 1, float(d[0]), float(d[1]), float(d[2])))
+            if not np.all(np.isfinite(d)):
+                raise NumericalFailureError("non-finite Newton residual in the finite-mu solve")
+            if d[0] < params.xi and d[1] < params.xi and d[2] < params.xi:
+                x = gx.clone()
+                converged = True
+                break
+            if step > max_newton:
+                break
+            xnorm = dot(x, x) ** 0.5
+
+            def jv(v):
+                nv = dot(v, v) ** 0.5
+                if nv == 0.0:
+                    return torch.zeros_like(v)
+                h = fd_eps * (1.0 + xnorm) / nv
+                return (g(x + h * v, gp) - gx) / h - v
+
+            rtol = min(0.1, max(1e-4, float(d.max())))
+            dx, its = _gmres_real(jv, -F, rtol, restart, max_restarts, dot)
+            report.steps.append((step, float(d[0]), float(d[1]), float(d[2]), its))
+            # backtracking on |F|_2: halve the step while the residual grows
+            fn = dot(F, F)
+            lam = 1.0
+            for _ls in range(line_search):
+                g(x + lam * dx, gp)
+                Ft = gp - (x + lam * dx)
+                if dot(Ft, Ft) < fn:
+                    break
+                lam *= 0.5
+            x = x + lam * dx
+        report.sweeps = sweeps[0]
+    finally:
+        if own:
+            sw.close()
+    xs = x.cpu().numpy()
+    A, B, C = (xs[k * n:(k + 1) * n].reshape(shape).copy() for k in range(3))
+    sol = MuSolution(A=A, B=B, C=C, iterations=len(hist) - 1, converged=converged, history=hist, grid=grid,
+                     params=params)
+    return sol, report
 
 
 def interp_mu(grid: MuGrid, F, params: MuParams | None = None, device: int = 0) -> np.ndarray:

@@ -420,3 +420,43 @@ def test_batch_sharded_world1_equals_standalone():
         assert mu_r == m and its == one.iterations and conv == one.converged
         for x, y in ((A, one.A), (B, one.B), (C, one.C)):
             assert np.array_equal(x.view(np.float64), y.view(np.float64))
+
+
+@pytest.mark.parametrize("mu", [0.0, 0.2])
+def test_newton_solves_full_bc_vertex_on_small_grids(mu):
+    """The full in-medium Ball-Chiu vertex diverges under successive
+    approximation; solve_mu_newton (Newton-Krylov on g(x) - x, device
+    sweeps) converges it on small grids, and the result is a fixed point of
+    the ORACLE's map: max|g_oracle(x) - x| within the stop tolerance
+    (conditioning-independent check of the GPU solution)."""
+    from paper_2012_03667_b200.finite_mu import solve_mu_newton
+    p = MuParams(vertex="bc", mu=mu, xi=1e-10, n_s=12, n_4=12, m_s=16, m_4=16, m_ang=8)
+    g = grid_for(p)
+    sol, rep = solve_mu_newton(p, g)
+    assert sol.converged and sol.iterations <= 10 and rep.start_iterations > 0
+    out = mu_oracle.sweep_rows_c(g, p, sol.A, sol.B, sol.C, np.arange(g.n_ext))
+    for c, F in enumerate((sol.A, sol.B, sol.C)):
+        assert np.max(np.abs(out[:, c] - F.reshape(-1))) < 1e-9
+    # successive approximation does not converge on the same problem (it
+    # runs to the cap or overflows into a numerical failure)
+    try:
+        sa = solve_mu(MuParams(**{**p.__dict__, "max_iterations": 300}), g)
+        assert not sa.converged
+    except NumericalFailureError:
+        pass
+
+
+def test_newton_reaches_the_successive_approximation_fixed_point():
+    """On the convergent 'bcb' vertex, Newton-Krylov started (start=None)
+    from the 10th successive-approximation iterate lands on solve_mu's fixed
+    point.  (From the raw initial guess A = C = 1, B = 0.3 it can land on a
+    different solution of the same equations: the gap equation has several.)"""
+    from paper_2012_03667_b200.finite_mu import solve_mu_newton
+    p = MuParams(vertex="bcb", mu=0.2, xi=1e-11, max_iterations=300, **SMALL)
+    g = grid_for(p)
+    sa = solve_mu(p, g)
+    s10 = solve_mu(MuParams(**{**p.__dict__, "max_iterations": 10}), g)
+    nk, rep = solve_mu_newton(p, g, s10.A, s10.B, s10.C, start=None)
+    assert sa.converged and nk.converged and rep.start_iterations == 0 and rep.sweeps > 0
+    for x, y in ((nk.A, sa.A), (nk.B, sa.B), (nk.C, sa.C)):
+        assert np.max(np.abs(x - y)) <= 1e-9 * np.max(np.abs(y))
