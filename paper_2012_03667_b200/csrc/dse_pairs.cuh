@@ -32,12 +32,21 @@
 // and finalises the row (partials in order (g, c)).  Results are bitwise independent of the grid size,
 // the schedule and the row sharding.
 
-constexpr int kPairsThreads = 256;
+// One CTA of 20 warps per SM (<= 102 registers, 5 warps per scheduler) with
+// the angular loop unrolled 4x: 0.330 ms at config 2 against 0.342 for two
+// CTAs of 8 warps unrolled 8x (118 registers).  Warps per SM that are not a
+// multiple of 4 load the schedulers unevenly (18: 0.347-0.361, 22: 0.342-0.352);
+// 24 warps at 80 registers 0.340; 16 warps in one CTA 0.338 (round 2, fourth
+// session; scripts/r02vc.sh, r02vd.sh).
+#ifndef DSE_PAIRS_THREADS
+#define DSE_PAIRS_THREADS 640
+#endif
+constexpr int kPairsThreads = DSE_PAIRS_THREADS;
 #ifndef DSE_PAIRS_MINB
-#define DSE_PAIRS_MINB 2  // 3 (80 regs) 0.359, 4 (64 regs) 0.367 ms: occupancy is not the limit
+#define DSE_PAIRS_MINB 1  // (256 threads: 2 CTAs 0.342, 3 (80 regs) 0.359, 4 (64 regs) 0.367 ms)
 #endif
 #ifndef DSE_PAIRS_UNROLL
-#define DSE_PAIRS_UNROLL 8  // measured at config 2: 2 -> 0.368, 4 -> 0.356, 8 -> 0.351 ms
+#define DSE_PAIRS_UNROLL 4  // 20 warps as 2 x 320: 2 -> 0.360, 3 -> 0.349, 4 -> 0.336; as 1 x 640: 4 -> 0.330, 8 -> 0.335 ms
 #endif
 constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
 // (sharing one exp between the symmetric angles z, -z -- exp(-kappa(-z)/w2)
@@ -73,6 +82,33 @@ constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
 // 6e-11 vs 3e-12 at config 0): the subtraction reintroduces the cancellation
 // that accumulating r-weighted moments avoids.  Not built.)
 
+// Where the time goes (ncu source page, round 2, profiles/r02/SUMMARY.md): 83%
+// of the warp samples sit in the angular loop, where the FP64 pipe runs at
+// ~87% (stalls: pipe throttle 30%, not selected 27%, fixed-latency wait 21%);
+// the other 17% are per-item work (ticket and the dependent loads 6.6%, fence
+// 1.7%, row constants / coefficients / reduction ~6%) and the wait at the grid
+// barrier (2.6%), and with 5 warps per scheduler every warp outside the loop
+// costs pipe time.  Per launch 0.2246 ms is the pipe's floor (23.42 FP64
+// instructions per point).  The loop's schedule is sensitive to the code
+// around it: builds whose loop differs only in register allocation run
+// 0.330-0.344 ms (the fixed-latency wait goes 21% -> 32%), so A/B differences
+// under ~4% between structurally different builds are not evidence.
+// Measured and not kept in that session (all bitwise or within the parity
+// bars, all slower than 0.330 ms at 640 x 1, unroll 4):
+//  - static schedule: every warp an equal contiguous share of the (row, group,
+//    chunk) sequence, no tickets, row constants once per row: 0.346-0.354 ms
+//    -- warps of one scheduler do not progress alike, the early finishers
+//    leave the pipe under-filled;
+//  - guided self-scheduling (a batch = 1/(2 warps) of the units left, down to
+//    single chunks): 0.340-0.346 ms at best, 0.36+ with 2-4 chunks per group
+//    (each extra item costs ~1.5 us of warp time, more than the level finish
+//    returns);
+//  - a quarter of the rows cut into 4 angle chunks scheduled last: +3 to +10%;
+//  - the finishing warp loading the row's partials side by side: 0.341 ms;
+//    items only for the groups inside the window (the finishing warp
+//    evaluating the outside ones in the non-finite case): 0.342 ms;
+//  - the angular loop as a __noinline__ function (a schedule independent of
+//    the surrounding code): 0.344 ms.
 __global__ void __launch_bounds__(kPairsThreads, DSE_PAIRS_MINB) dse_pairs_kernel(SweepArgs a) {
     if (a.stop && *a.stop) return;  // sharded solve already stopped (uniform over the grid)
     cg::grid_group grid = cg::this_grid();
