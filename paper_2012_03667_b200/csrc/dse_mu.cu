@@ -93,7 +93,10 @@ struct MuArgs {
     long long mo_stride;
 };
 
-constexpr int kThreads = 256;
+#ifndef DSE_MU_THREADS
+#define DSE_MU_THREADS 256
+#endif
+constexpr int kThreads = DSE_MU_THREADS;
 constexpr int kWarps = kThreads / 32;
 #ifndef DSE_MU_UNROLL
 #define DSE_MU_UNROLL 8  // config 3, bcb: unroll 2 5.46, 4 5.52, 8 5.35 ms; 3 CTAs/SM (80 regs) 5.51 ms
@@ -105,6 +108,10 @@ constexpr int kMuUnroll = DSE_MU_UNROLL;
 constexpr bool kMuMirror = DSE_MU_MIRROR;
 #ifndef DSE_MU_MINB
 #define DSE_MU_MINB 2  // CTAs per SM the register budget is cut for (A/B: scripts/mu_ab.sh)
+// (20 warps per SM, which pays in the vacuum pairs kernel, does not here: at the
+// 102-register cap these kernels spill 140-476 B -- config 3 direct / moments
+// sweep 4.69 / 1.63 ms at 256 x 2; 320 x 2: 5.13-5.28 / 2.18; 640 x 1: 5.50-5.65 /
+// 2.77; 512 x 1 (128 registers): 5.02 / 1.93 -- round 2, scripts/r02vo.sh)
 #endif
 
 // clamped linear rule of the reference along one axis (interpolation.py:71-72, :125-132)
