@@ -92,7 +92,9 @@ constexpr int kPairsUnroll = DSE_PAIRS_UNROLL;
 // instructions per point).  The loop's schedule is sensitive to the code
 // around it: builds whose loop differs only in register allocation run
 // 0.330-0.344 ms (the fixed-latency wait goes 21% -> 32%), so A/B differences
-// under ~4% between structurally different builds are not evidence.
+// under ~4% between structurally different builds are not evidence.  (The same
+// operations in two other source orders: 0.338, 0.339 ms; a register cap of 80
+// through a larger launch bound: 0.347 ms -- this build's schedule is a good one.)
 // Measured and not kept in that session (all bitwise or within the parity
 // bars, all slower than 0.330 ms at 640 x 1, unroll 4):
 //  - static schedule: every warp an equal contiguous share of the (row, group,
