@@ -85,6 +85,9 @@ def test_pairs_grid_size_bitwise_equal(n, m, k):
     for blocks in ("1", "7", "150"):
         x = _sweep(g, prm, {"DSE_PAIRS_BLOCKS": blocks}, p.Arithmetic.PAIRS)
         assert np.array_equal(ref[0], x[0]) and np.array_equal(ref[1], x[1]), blocks
+    for threads in ("640", "320", "96"):  # the launch shape (one CTA of 640 / two of 320 by problem size)
+        x = _sweep(g, prm, {"DSE_PAIRS_LAUNCH_THREADS": threads}, p.Arithmetic.PAIRS)
+        assert np.array_equal(ref[0], x[0]) and np.array_equal(ref[1], x[1]), threads
     for chunks in ("2", "4"):  # angle chunks change the partition, not the result beyond rounding
         x = _sweep(g, prm, {"DSE_PAIRS_CHUNKS": chunks}, p.Arithmetic.PAIRS)
         assert np.max(np.abs(ref[0] - x[0]) / np.abs(ref[0])) < 1e-13
